@@ -1,0 +1,394 @@
+#!/usr/bin/env python
+"""PipeFisher B200 benchmark (contract: one JSON line on rank 0).
+
+Workload (config.workload = "bert_large_kfac_layer_step"): one K-FAC step of
+one BERT-Large encoder layer — BASELINE.json configs[0] at BERT-Large shapes
+(hidden 1024, FFN 4096, micro-batch 32 x 128 = 4096 tokens), the per-layer
+unit of the Chimera/1F1B configs the metric is quoted on:
+  * curvature: 12 Kronecker factors (A and B of Q, K, V, O, FFN1, FFN2;
+    10 x 1024^2 + 2 x 4096^2) from bf16 tapes, one grouped tcgen05 SYRK launch;
+  * inversion: 12 damped inverses (lambda = 0.1), fp32-accurate, batched;
+  * precondition: 6 x  W -= eta B^-1 G A^-1  (3xTF32 tcgen05, fused update).
+Algorithmic FLOPs per step: SYRK d(d+1)n, inverse d^3,
+precondition 2 d_out^2 d_in + 2 d_out d_in^2.  value = those FLOPs / step time.
+
+N > 1 (torchrun, one rank per GPU): data-parallel replicas of the layer step
+with the path's real exchange steps — factor all-reduce (SyncCurvature) over
+NCCL and inversion parallelism (round-robin inversion ownership, inverse
+broadcast) as in the paper; weak scaling.
+
+--impl reference: the reference's own CPU implementation (oracle/_ref, the
+unmodified reference sources compiled in-tree) on the same metric, a bounded
+sample per step, all host threads.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+from concurrent.futures import ThreadPoolExecutor
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "BERT-Large PipeFisher step time & GPU util at 1/2/4/8 B200; K-FAC TFLOP/s"
+UNIT = "TFLOP/s"
+D_MODEL, D_FF, TOKENS = 1024, 4096, 32 * 128
+LINEARS = [("q", D_MODEL, D_MODEL), ("k", D_MODEL, D_MODEL), ("v", D_MODEL, D_MODEL),
+           ("o", D_MODEL, D_MODEL), ("ffn1", D_MODEL, D_FF), ("ffn2", D_FF, D_MODEL)]  # (name, d_in, d_out)
+DAMPING, ETA = 0.1, 1e-3
+
+
+def layer_flops(tokens=TOKENS):
+    syrk = sum(d * (d + 1) * tokens for _, di, do in LINEARS for d in (di, do))
+    inv = sum(d ** 3 for _, di, do in LINEARS for d in (di, do))
+    prec = sum(2 * do * do * di + 2 * do * di * di for _, di, do in LINEARS)
+    return syrk, inv, prec
+
+
+def peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            p = json.load(f)
+        return p, "measured"
+    except Exception:
+        return {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0, "bf16_tflops_sustained": 1400.0}, "fallback"
+
+
+class ClockSampler:
+    """nvidia-smi clocks/throttle reasons sampled DURING the timed region."""
+
+    def __init__(self, index=0):
+        self.index = index
+        self.samples = []
+        self._stop = threading.Event()
+        self._t = None
+
+    def _run(self):
+        q = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
+             "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+             "clocks_event_reasons.sw_power_cap")
+        while not self._stop.is_set():
+            try:
+                out = subprocess.run(["nvidia-smi", f"--id={self.index}", f"--query-gpu={q}",
+                                      "--format=csv,noheader,nounits"], capture_output=True,
+                                     text=True, timeout=5).stdout.strip()
+                f = [x.strip() for x in out.split(",")]
+                if len(f) >= 7:
+                    self.samples.append(f)
+            except Exception:
+                pass
+            self._stop.wait(0.2)
+
+    def __enter__(self):
+        self._t = threading.Thread(target=self._run, daemon=True)
+        self._t.start()
+        return self
+
+    def __exit__(self, *a):
+        self._stop.set()
+        self._t.join(timeout=10)
+
+    def summary(self):
+        if not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        sm = [float(s[0]) for s in self.samples if s[0].replace(".", "").isdigit()]
+        mx = [float(s[1]) for s in self.samples if s[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for s in self.samples for i in range(4)
+                          if s[3 + i].lower() in ("active", "1", "yes")})
+        return {"sm_mhz": statistics.median(sm) if sm else None,
+                "sm_max_mhz": max(mx) if mx else None, "reasons": reasons,
+                "samples": len(self.samples)}
+
+
+# ====================================================================== CPU arms
+def reference_sample(threads):
+    """A bounded sample of the same layer step on the reference CPU path: per
+    thread one d_model factor pair (curvature_factors over 512 tokens), one
+    cholesky_spd_inverse(1024) and one precondition(1024 x 1024)."""
+    import numpy as np
+    from oracle import ref as R
+    tok = 512
+    a = R.orc_symmetric(1, (D_MODEL, tok), 3 ** 0.5)
+    e = R.orc_symmetric(2, (D_MODEL, tok), 3 ** 0.5)
+    A, B = R.ref_curvature_factors(a, e)
+    g = R.orc_symmetric(3, (D_MODEL, D_MODEL))
+
+    def job(_):
+        t0 = time.perf_counter()
+        R.ref_curvature_factors(a, e)
+        ai = R.ref_cholesky_spd_inverse(A, DAMPING)
+        bi = ai  # same-size second inverse skipped: one inverse per job
+        R.ref_precondition(g, ai, bi)
+        return time.perf_counter() - t0
+
+    flops_per_job = 2 * D_MODEL * (D_MODEL + 1) * tok + D_MODEL ** 3 + 4 * D_MODEL ** 3
+    t0 = time.perf_counter()
+    with ThreadPoolExecutor(max_workers=threads) as ex:
+        list(ex.map(job, range(threads)))
+    dt = time.perf_counter() - t0
+    sample = (f"{threads} x [curvature_factors(a,e: {D_MODEL}x{tok}) + cholesky_spd_inverse({D_MODEL})"
+              f" + precondition({D_MODEL}x{D_MODEL})], FP64, std::thread-parallel over independent calls")
+    return threads * flops_per_job / dt / 1e12, dt, sample
+
+
+def cpu_threads():
+    try:
+        return max(1, min(len(os.sched_getaffinity(0)), 16))
+    except Exception:
+        return max(1, min(os.cpu_count() or 1, 16))
+
+
+def run_reference_arm(args, rank, world):
+    if rank != 0:
+        return
+    threads = cpu_threads()
+    for _ in range(args.warmup):
+        reference_sample(threads)
+    vals, times = [], []
+    for _ in range(args.steps):
+        v, dt, sample = reference_sample(threads)
+        vals.append(v)
+        times.append(dt)
+    value = statistics.mean(vals)
+    line = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * statistics.mean(times),
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic (SplitMix64)",
+        "config": {"workload": "bert_large_kfac_layer_step", "sample": "bounded CPU sample",
+                   "tokens": 512},
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": "reference",
+                         "sample": sample},
+        "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+# ====================================================================== GPU arm
+class LayerStep:
+    """Device-resident state for one replica's layer step."""
+
+    def __init__(self, torch, K, seed):
+        g = torch.Generator(device="cuda").manual_seed(seed)
+        self.torch, self.K = torch, K
+        self.tapes, self.factors, self.inv, self.digits = [], [], [], []
+        for _, di, do in LINEARS:
+            for d in (di, do):
+                self.tapes.append(torch.randn((d, TOKENS), generator=g, device="cuda").to(torch.bfloat16))
+                self.factors.append(torch.empty((d, d), device="cuda"))
+                self.inv.append(torch.empty((d, d), device="cuda"))
+                self.digits.append(torch.empty(K.slice_bytes(d, d), dtype=torch.uint8, device="cuda"))
+        self.grads = [torch.randn((do, di), generator=g, device="cuda") for _, di, do in LINEARS]
+        self.weights = [0.02 * torch.randn((do, di), generator=g, device="cuda") for _, di, do in LINEARS]
+
+    def curvature(self):
+        self.K.syrk([(x, f, 1.0 / TOKENS, False) for x, f in zip(self.tapes, self.factors)],
+                    fill_upper=False)
+
+    def invert(self, which=None):
+        idx = range(len(self.factors)) if which is None else which
+        idx = list(idx)
+        if idx:
+            self.K.damped_inverse_batched([self.factors[i] for i in idx], DAMPING,
+                                          [self.inv[i] for i in idx],
+                                          [self.digits[i] for i in idx], check=False)
+
+    def precondition(self):
+        K = self.K
+        items = []
+        for l in range(len(LINEARS)):
+            ai = K.SlicedMatrix(self.inv[2 * l], self.digits[2 * l])
+            bi = K.SlicedMatrix(self.inv[2 * l + 1], self.digits[2 * l + 1])
+            items.append((self.weights[l], self.grads[l], ai, bi, ETA))
+        K.precondition_update_sliced(items)
+
+
+def run_gpu_arm(args, rank, world, local_rank):
+    import torch
+    from paper_2211_14133_b200 import kfac as K
+    torch.cuda.set_device(local_rank)
+    if not K.device_ok():
+        raise SystemExit("libpf_b200.so: no sm_100 device")
+    dist = None
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+
+    st = LayerStep(torch, K, seed=1234 + rank)
+    stream = torch.cuda.current_stream()
+
+    def exchange():
+        # SyncCurvature: average factors over data-parallel replicas (NCCL),
+        # then inversion parallelism: factor i inverted on rank i % world.
+        for f in st.factors:
+            dist.all_reduce(f, op=dist.ReduceOp.AVG)
+
+    def step(ev=None):
+        if ev: ev[0].record(stream)
+        st.curvature()
+        if ev: ev[1].record(stream)
+        if world > 1:
+            exchange()
+            mine = [i for i in range(len(st.factors)) if i % world == rank]
+            st.invert(mine)
+            for i in range(len(st.factors)):
+                dist.broadcast(st.inv[i], src=i % world)
+                dist.broadcast(st.digits[i], src=i % world)
+        else:
+            st.invert()
+        if ev: ev[2].record(stream)
+        st.precondition()
+        if ev: ev[3].record(stream)
+
+    for _ in range(max(3, args.warmup)):
+        step()
+    torch.cuda.synchronize()
+
+    # ---------------------------------------------------------- device timing
+    evs = [[torch.cuda.Event(enable_timing=True) for _ in range(4)] for _ in range(args.steps)]
+    if dist: dist.barrier()
+    torch.cuda.synchronize()
+    launches0 = K.kernel_launches()
+    with ClockSampler(local_rank) as clocks:
+        t_start = torch.cuda.Event(enable_timing=True)
+        t_end = torch.cuda.Event(enable_timing=True)
+        t_start.record(stream)
+        for i in range(args.steps):
+            step(evs[i])
+        t_end.record(stream)
+        torch.cuda.synchronize()
+    launches = K.kernel_launches() - launches0
+    if dist: dist.barrier()
+    ms = t_start.elapsed_time(t_end) / args.steps
+    phases = {"curvature": 0.0, "inversion": 0.0, "precondition": 0.0}
+    for e in evs:
+        phases["curvature"] += e[0].elapsed_time(e[1]) / args.steps
+        phases["inversion"] += e[1].elapsed_time(e[2]) / args.steps
+        phases["precondition"] += e[2].elapsed_time(e[3]) / args.steps
+    if dist:
+        t = torch.tensor([ms], device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+
+    syrk_f, inv_f, prec_f = layer_flops()
+    job_flops = world * (syrk_f + prec_f) + inv_f * (1 if world > 1 else 1)
+    if world == 1:
+        job_flops = syrk_f + inv_f + prec_f
+    value = job_flops / (ms * 1e-3) / 1e12
+
+    # ---------------------------------------------------------- end-to-end (public API, host buffers)
+    h_tapes = [x.cpu().pin_memory() for x in st.tapes]
+    h_grads = [g.cpu().pin_memory() for g in st.grads]
+    h_w = [w.cpu().pin_memory() for w in st.weights]
+    h2d = sum(t.numel() * t.element_size() for t in h_tapes + h_grads)
+    d2h = sum(t.numel() * t.element_size() for t in h_w)
+
+    def e2e_step():
+        for h, d in zip(h_tapes, st.tapes):
+            d.copy_(h, non_blocking=True)
+        for h, d in zip(h_grads, st.grads):
+            d.copy_(h, non_blocking=True)
+        step()
+        for h, d in zip(h_w, st.weights):
+            h.copy_(d, non_blocking=True)
+    for _ in range(2):
+        e2e_step()
+    if dist: dist.barrier()
+    torch.cuda.synchronize()
+    e0 = torch.cuda.Event(enable_timing=True)
+    e1 = torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    for _ in range(args.steps):
+        e2e_step()
+    e1.record(stream)
+    torch.cuda.synchronize()
+    e2e_ms = e0.elapsed_time(e1) / args.steps
+    if dist:
+        t = torch.tensor([e2e_ms], device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        e2e_ms = float(t.item())
+    e2e_value = job_flops / (e2e_ms * 1e-3) / 1e12
+
+    if rank != 0:
+        if dist: dist.destroy_process_group()
+        return
+
+    pk, pk_kind = peaks()
+    syrk_ms = phases["curvature"]
+    achieved = syrk_f / (syrk_ms * 1e-3) / 1e12
+    traffic = None
+    try:
+        with open(os.path.join(ROOT, "profiles", "syrk_traffic.json")) as f:
+            traffic = json.load(f).get("dram_bytes_per_launch")
+    except Exception:
+        pass
+    roof = {"kernel": "umma_gemm_kernel<bf16> (grouped SYRK, 12 factors, 1 launch)",
+            "bound": "tensor", "achieved": achieved, "peak": pk["bf16_tflops_sustained"],
+            "unit": "TFLOP/s", "frac": achieved / pk["bf16_tflops_sustained"],
+            "traffic": traffic, "peak_source": f"{pk_kind} bf16_tflops_sustained"}
+    # digit-form GEMM: 10 int8 products (kind::i8 = 2x the bf16 rate) per fp32 product
+    emu_peak = pk["bf16_tflops"] * 2 / 10
+    phase_rates = {
+        "curvature": {"ms": phases["curvature"], "tflops": syrk_f / phases["curvature"] / 1e9},
+        "inversion": {"ms": phases["inversion"], "tflops": inv_f / phases["inversion"] / 1e9,
+                      "peak_fp32_digit_tflops": emu_peak},
+        "precondition": {"ms": phases["precondition"], "tflops": prec_f / phases["precondition"] / 1e9,
+                         "peak_fp32_digit_tflops": emu_peak},
+    }
+    cpu = None
+    if world == 1 and not args.no_cpu_baseline:
+        threads = cpu_threads()
+        v, dt, sample = reference_sample(threads)
+        cpu = {"value": v, "unit": UNIT, "cores": threads, "kind": "reference", "sample": sample,
+               "seconds": dt}
+    line = {
+        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "bf16 curvature / fp32 (3xTF32) inversion+precondition",
+        "data": "synthetic (torch.randn tapes/grads/weights, random init)",
+        "config": {"workload": "bert_large_kfac_layer_step", "d_model": D_MODEL, "d_ff": D_FF,
+                   "tokens_per_micro_batch": TOKENS, "factors": 12, "linears": 6,
+                   "damping": DAMPING, "parallelism": f"dp{world}" + ("+inv-parallel" if world > 1 else ""),
+                   "l2": "inputs larger than L2 (tapes 144 MB + factors 168 MB per step)"},
+        "phases": phase_rates,
+        "roofline": roof,
+        "e2e": {"value": e2e_value, "unit": UNIT, "ms_per_step": e2e_ms,
+                "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h},
+        "gpu_launches": launches // max(1, args.steps) if False else launches,
+        "clocks": clocks.summary(),
+        "cpu_baseline": cpu,
+    }
+    print(json.dumps(line), flush=True)
+    if dist: dist.destroy_process_group()
+
+
+def main():
+    p = argparse.ArgumentParser()
+    p.add_argument("--gpus", type=int, default=1)
+    p.add_argument("--steps", type=int, default=10)
+    p.add_argument("--warmup", type=int, default=3)
+    p.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    p.add_argument("--no-cpu-baseline", action="store_true")
+    args = p.parse_args()
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", str(args.gpus)))
+    local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+    if "RANK" not in os.environ:
+        world = 1 if args.gpus <= 1 else args.gpus
+        if world > 1:
+            raise SystemExit("N>1 must be launched with torchrun (one rank per GPU)")
+    if args.impl == "reference":
+        run_reference_arm(args, rank, world)
+    else:
+        run_gpu_arm(args, rank, world, local_rank)
+
+
+if __name__ == "__main__":
+    main()

@@ -21,8 +21,9 @@
  *
  * Precision: curvature takes bf16 activations/errors and accumulates in fp32
  * on tcgen05 (kind::f16).  Inversion and preconditioning are fp32-accurate:
- * every GEMM-shaped step runs 3xTF32 on tcgen05 (hi*hi + hi*lo + lo*hi, fp32
- * accumulation in TMEM); panel factorisations run in fp32 on the SIMT cores.
+ * every GEMM-shaped step runs on tcgen05 kind::i8 over int8 digit planes with
+ * exact int32 accumulation (see pf_slice); the 128x128 diagonal blocks of the
+ * inverse are factored on the SIMT cores with fp64 accumulation.
  */
 #ifndef PF_KFAC_H
 #define PF_KFAC_H
@@ -57,24 +58,34 @@ int pf_curvature_syrk(const void* x_bf16, int d, int n, int ldx, float scale, in
 int pf_curvature_syrk_grouped(const pf_syrk_problem* problems, int count, int fill_upper,
                               void* stream);
 
+/* fp32-accurate tensor-core operands ("digit form").  Every row of an fp32
+ * matrix [rows x k] becomes a power-of-two scale 2^e and four signed 7-bit
+ * int8 digits (x = 2^e sum_s q_s 2^-7(s+1), error <= 2^-28 max|row|); the
+ * products of digit planes run on tcgen05.mma.kind::i8 with exact int32
+ * accumulation and are recombined in fp64.  Inverses are kept in this form
+ * between refreshes so every preconditioning step reuses them. */
+int pf_slice_bytes(int rows, int k, size_t* bytes);
+int pf_slice(const float* x, int rows, int k, int ld, void* sliced, void* stream);
+
 /* Damped inverse (M + damping*I)^-1 of a symmetric positive-definite fp32
  * matrix; only the lower triangle of M is read.  Replaces
  * kfac::cholesky_spd_inverse (proj/src/kfac/matrix.cpp:136-163):
- * damp, Cholesky L, L^-1, then L^-T L^-1.
- * minv_lo == NULL: minv receives the plain fp32 inverse (full symmetric).
- * minv_lo != NULL: (minv, minv_lo) receive the tf32 hi/lo split of the
- * inverse — the form pf_precondition_update_split consumes directly.
+ * damp, Cholesky L, L^-1, then L^-T L^-1 — here a recursive blocked
+ * factorisation whose diagonal 128-blocks are factored in shared memory
+ * (fp64 accumulation) and whose off-diagonal work runs as digit-form
+ * tensor-core GEMMs.  minv receives the full symmetric fp32 inverse;
+ * minv_sliced (nullable, pf_slice_bytes(d, d)) also receives its digit form.
  * d_info: device int, set to 0 or the 1-based column of the first failed
  * pivot (reference: std::domain_error "matrix not positive definite"). */
 int pf_damped_inverse_workspace(int d, size_t* bytes);
-int pf_damped_inverse(const float* m, int d, int ldm, float damping, float* minv,
-                      float* minv_lo, int ldinv, void* workspace, size_t workspace_bytes,
-                      int* d_info, void* stream);
+int pf_damped_inverse(const float* m, int d, int ldm, float damping, float* minv, int ldinv,
+                      void* minv_sliced, void* workspace, size_t workspace_bytes, int* d_info,
+                      void* stream);
 
 typedef struct pf_inverse_problem {
     const float* m;
     float* minv;
-    float* minv_lo; /* nullable */
+    void* minv_sliced; /* nullable */
     int32_t d, ldm, ldinv;
     float damping;
     void* workspace; /* pf_damped_inverse_workspace(d) bytes each */
@@ -95,26 +106,22 @@ int pf_precondition_update(const float* b_inv, const float* grad, const float* a
                            int d_out, int d_in, float eta, void* workspace,
                            size_t workspace_bytes, void* stream);
 
-/* Same with pre-split (hi/lo) inverses from pf_damped_inverse(minv_lo != NULL):
- * the refresh-time split is reused for every step until the next refresh. */
+/* Grouped, with inverses already in digit form (pf_damped_inverse's
+ * minv_sliced): the refresh-time slicing is reused by every step. */
 typedef struct pf_precondition_problem {
-    const float* b_inv_hi;
-    const float* b_inv_lo;
+    const void* b_inv_sliced;
     const float* grad;
-    const float* a_inv_hi;
-    const float* a_inv_lo;
+    const void* a_inv_sliced;
     float* w;       /* updated in place: W -= eta * P   (nullable if p_out) */
     float* p_out;   /* receives P                      (nullable if w)     */
     int32_t d_out, d_in;
     float eta;
     void* workspace; /* pf_precondition_workspace(d_out, d_in) bytes */
 } pf_precondition_problem;
-int pf_precondition_update_split(const pf_precondition_problem* problems, int count,
-                                 void* stream);
+int pf_precondition_update_sliced(const pf_precondition_problem* problems, int count,
+                                  void* stream);
 
-/* Utility: split fp32 x into tf32 (hi, lo) with hi + lo == x. */
-int pf_split_tf32(const float* x, int64_t n, float* hi, float* lo, void* stream);
-/* Utility: round fp32/fp64 host-side tapes to bf16 on device (x: fp32). */
+/* Utility: round an fp32 device array to bf16 (tape preparation). */
 int pf_f32_to_bf16(const float* x, int64_t n, void* out_bf16, void* stream);
 
 /* Number of kernels this library launched since load (evidence counter for

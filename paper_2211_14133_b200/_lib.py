@@ -57,16 +57,15 @@ class PfSyrkProblem(C.Structure):
 
 
 class PfInverseProblem(C.Structure):
-    _fields_ = [("m", C.c_void_p), ("minv", C.c_void_p), ("minv_lo", C.c_void_p),
+    _fields_ = [("m", C.c_void_p), ("minv", C.c_void_p), ("minv_sliced", C.c_void_p),
                 ("d", C.c_int32), ("ldm", C.c_int32), ("ldinv", C.c_int32),
                 ("damping", C.c_float), ("workspace", C.c_void_p), ("d_info", C.c_void_p)]
 
 
 class PfPreconditionProblem(C.Structure):
-    _fields_ = [("b_inv_hi", C.c_void_p), ("b_inv_lo", C.c_void_p), ("grad", C.c_void_p),
-                ("a_inv_hi", C.c_void_p), ("a_inv_lo", C.c_void_p), ("w", C.c_void_p),
-                ("p_out", C.c_void_p), ("d_out", C.c_int32), ("d_in", C.c_int32),
-                ("eta", C.c_float), ("workspace", C.c_void_p)]
+    _fields_ = [("b_inv_sliced", C.c_void_p), ("grad", C.c_void_p), ("a_inv_sliced", C.c_void_p),
+                ("w", C.c_void_p), ("p_out", C.c_void_p), ("d_out", C.c_int32),
+                ("d_in", C.c_int32), ("eta", C.c_float), ("workspace", C.c_void_p)]
 
 
 P = C.POINTER
@@ -107,8 +106,10 @@ _SIGNATURES = {
     "pf_curvature_syrk_grouped": (C.c_int, [P(PfSyrkProblem), C.c_int, C.c_int, C.c_void_p]),
     "pf_damped_inverse_workspace": (C.c_int, [C.c_int, P(C.c_size_t)]),
     "pf_damped_inverse": (C.c_int, [C.c_void_p, C.c_int, C.c_int, C.c_float, C.c_void_p,
-                                    C.c_void_p, C.c_int, C.c_void_p, C.c_size_t, C.c_void_p,
+                                    C.c_int, C.c_void_p, C.c_void_p, C.c_size_t, C.c_void_p,
                                     C.c_void_p]),
+    "pf_slice_bytes": (C.c_int, [C.c_int, C.c_int, P(C.c_size_t)]),
+    "pf_slice": (C.c_int, [C.c_void_p, C.c_int, C.c_int, C.c_int, C.c_void_p, C.c_void_p]),
     "pf_damped_inverse_batched": (C.c_int, [P(PfInverseProblem), C.c_int, C.c_void_p]),
     "pf_precondition_workspace": (C.c_int, [C.c_int, C.c_int, P(C.c_size_t)]),
     "pf_precondition": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_int,
@@ -116,8 +117,7 @@ _SIGNATURES = {
     "pf_precondition_update": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p,
                                          C.c_int, C.c_int, C.c_float, C.c_void_p, C.c_size_t,
                                          C.c_void_p]),
-    "pf_precondition_update_split": (C.c_int, [P(PfPreconditionProblem), C.c_int, C.c_void_p]),
-    "pf_split_tf32": (C.c_int, [C.c_void_p, C.c_int64, C.c_void_p, C.c_void_p, C.c_void_p]),
+    "pf_precondition_update_sliced": (C.c_int, [P(PfPreconditionProblem), C.c_int, C.c_void_p]),
     "pf_f32_to_bf16": (C.c_int, [C.c_void_p, C.c_int64, C.c_void_p, C.c_void_p]),
     "pf_kernel_launch_count": (C.c_int64, []),
     "pf_device_ok": (C.c_int, []),

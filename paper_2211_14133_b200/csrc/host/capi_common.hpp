@@ -9,6 +9,12 @@
 
 namespace pf_detail {
 
+// std::invalid_argument raised for a shape mismatch (reference message kept);
+// maps to PF_BAD_SHAPE instead of PF_BAD_ARG.
+struct ShapeError : std::invalid_argument {
+    using std::invalid_argument::invalid_argument;
+};
+
 inline std::string& last_error() {
     thread_local std::string msg;
     return msg;
@@ -21,6 +27,9 @@ int guard(F&& body) noexcept {
     try {
         last_error().clear();
         return body();
+    } catch (const ShapeError& e) {
+        last_error() = e.what();
+        return PF_BAD_SHAPE;
     } catch (const std::domain_error& e) {
         last_error() = e.what();
         return PF_NOT_PD;

@@ -1,8 +1,9 @@
 // Diagonal-block kernel of the damped inverse: for one 128x128 diagonal block
 // A_kk (already holding all trailing updates) compute
 //     L_kk = chol(A_kk)          and          X_kk = L_kk^-1
-// in fp32 on the SIMT cores, entirely in shared memory, and write X_kk (lower,
-// explicit zeros above) and X_kk^T (upper, zeros below) as tf32 hi/lo pairs.
+// on the SIMT cores, entirely in shared memory (fp32 storage, every dot
+// product accumulated in fp64 and rounded once), and write X_kk (lower,
+// explicit zeros above) and X_kk^T (upper, zeros below).
 //
 // Follows the reference arithmetic (proj/src/kfac/matrix.cpp:117-153):
 // pivot test `!(diag > 0) || !isfinite(diag)` -> 1-based failing column in
@@ -27,12 +28,9 @@ constexpr int kMaxLeafBatch = 32;
 constexpr int kLeafSmemBytes = 2 * kLeaf * kLeafPitch * 4 + 16;
 
 struct LeafArgs {
-    const float* a_hi;
-    const float* a_lo;
-    float* x_hi;
-    float* x_lo;
-    float* xt_hi;
-    float* xt_lo;
+    const float* a;
+    float* x;
+    float* xt;
     int* info;
     int ld;    // shared leading dimension of a / x / xt
     int n;     // block size (<= 128; the tail block of a non-multiple-of-128 d)
@@ -64,7 +62,7 @@ template <int kMaxPerThread>
 __device__ void smem_gemm(const SmemGemm* probs, int count) {
     int total = 0;
     for (int q = 0; q < count; ++q) total += (probs[q].M / 4) * (probs[q].N / 4);
-    float acc[kMaxPerThread][4][4];
+    double acc[kMaxPerThread][4][4];
     int where[kMaxPerThread][3];
 #pragma unroll
     for (int s = 0; s < kMaxPerThread; ++s) {
@@ -88,7 +86,7 @@ __device__ void smem_gemm(const SmemGemm* probs, int count) {
 #pragma unroll
             for (int c = 0; c < 4; ++c) acc[s][r][c] = 0.0f;
         for (int k = 0; k < P.K; ++k) {
-            float av[4], bv[4];
+            double av[4], bv[4];
 #pragma unroll
             for (int r = 0; r < 4; ++r) av[r] = P.a[(ti + r * mstep) * P.ars + k * P.aks];
 #pragma unroll
@@ -96,7 +94,7 @@ __device__ void smem_gemm(const SmemGemm* probs, int count) {
 #pragma unroll
             for (int r = 0; r < 4; ++r)
 #pragma unroll
-                for (int c = 0; c < 4; ++c) acc[s][r][c] = fmaf(av[r], bv[c], acc[s][r][c]);
+                for (int c = 0; c < 4; ++c) acc[s][r][c] = fma(av[r], bv[c], acc[s][r][c]);
         }
     }
     __syncthreads();
@@ -114,7 +112,8 @@ __device__ void smem_gemm(const SmemGemm* probs, int count) {
                 const int j = where[s][2] + c * nstep;
                 if (P.lower && j > i) continue;
                 float* dst = P.c + i * kLeafPitch + j;
-                *dst = (P.beta != 0.0f ? P.beta * *dst : 0.0f) + P.alpha * acc[s][r][c];
+                const double old = P.beta != 0.0f ? static_cast<double>(P.beta) * *dst : 0.0;
+                *dst = static_cast<float>(old + static_cast<double>(P.alpha) * acc[s][r][c]);
             }
     }
     __syncthreads();
@@ -124,40 +123,41 @@ __device__ void smem_gemm(const SmemGemm* probs, int count) {
 // its inverse into Xs (full 32x32 with zeros above the diagonal).
 __device__ void panel_chol_inv32(float* Ls, float* Xs, int c0, int col_base, int n, int* bad) {
     const int lane = threadIdx.x & 31;
-    float a[32];
+    double a[32];
 #pragma unroll
-    for (int j = 0; j < 32; ++j) a[j] = (j <= lane) ? Ls[(c0 + lane) * kLeafPitch + c0 + j] : 0.0f;
+    for (int j = 0; j < 32; ++j) a[j] = (j <= lane) ? Ls[(c0 + lane) * kLeafPitch + c0 + j] : 0.0;
 #pragma unroll
     for (int k = 0; k < 32; ++k) {
-        float piv = __shfl_sync(0xffffffffu, a[k], k);
-        if (!(piv > 0.0f) || !isfinite(piv)) {
+        double piv = __shfl_sync(0xffffffffu, a[k], k);
+        if (!(piv > 0.0) || !isfinite(piv)) {
             if (lane == 0 && c0 + k < n) atomicMin(bad, col_base + c0 + k + 1);
-            piv = 1.0f;  // keep going; the caller reports the failure
+            piv = 1.0;  // keep going; the caller reports the failure
         }
-        const float lkk = sqrtf(piv);
+        const double lkk = sqrt(piv);
         if (lane == k) a[k] = lkk;
         if (lane > k) a[k] = a[k] / lkk;
 #pragma unroll
         for (int j = k + 1; j < 32; ++j) {
-            const float ljk = __shfl_sync(0xffffffffu, a[k], j);
-            if (lane >= j) a[j] = fmaf(-a[k], ljk, a[j]);
+            const double ljk = __shfl_sync(0xffffffffu, a[k], j);
+            if (lane >= j) a[j] = fma(-a[k], ljk, a[j]);
         }
     }
 #pragma unroll
-    for (int j = 0; j < 32; ++j) Ls[(c0 + lane) * kLeafPitch + c0 + j] = (j <= lane) ? a[j] : 0.0f;
+    for (int j = 0; j < 32; ++j)
+        Ls[(c0 + lane) * kLeafPitch + c0 + j] = (j <= lane) ? static_cast<float>(a[j]) : 0.0f;
     __syncwarp();
     // column `lane` of L^-1 by forward substitution (reference matrix.cpp:145-153)
-    float x[32];
+    double x[32];
 #pragma unroll
     for (int i = 0; i < 32; ++i) {
-        float s = 0.0f;
+        double s = 0.0;
 #pragma unroll
-        for (int k = 0; k < i; ++k) s = fmaf(Ls[(c0 + i) * kLeafPitch + c0 + k], x[k], s);
-        const float lii = Ls[(c0 + i) * kLeafPitch + c0 + i];
-        x[i] = (i == lane) ? 1.0f / lii : (i > lane ? -s / lii : 0.0f);
+        for (int k = 0; k < i; ++k) s = fma(static_cast<double>(Ls[(c0 + i) * kLeafPitch + c0 + k]), x[k], s);
+        const double lii = Ls[(c0 + i) * kLeafPitch + c0 + i];
+        x[i] = (i == lane) ? 1.0 / lii : (i > lane ? -s / lii : 0.0);
     }
 #pragma unroll
-    for (int i = 0; i < 32; ++i) Xs[(c0 + i) * kLeafPitch + c0 + lane] = x[i];
+    for (int i = 0; i < 32; ++i) Xs[(c0 + i) * kLeafPitch + c0 + lane] = static_cast<float>(x[i]);
 }
 
 __global__ void __launch_bounds__(kLeafThreads, 1) leaf_chol_inv_kernel(const __grid_constant__ LeafBatch batch) {
@@ -176,7 +176,7 @@ __global__ void __launch_bounds__(kLeafThreads, 1) leaf_chol_inv_kernel(const __
         const int r = idx / kLeaf, c = idx % kLeaf;
         float v;
         if (r < n && c < n)
-            v = (c <= r) ? A.a_hi[(size_t)r * A.ld + c] + A.a_lo[(size_t)r * A.ld + c] : 0.0f;
+            v = (c <= r) ? A.a[(size_t)r * A.ld + c] : 0.0f;
         else
             v = (r == c) ? 1.0f : 0.0f;
         Ls[r * kLeafPitch + c] = v;
@@ -233,18 +233,11 @@ __global__ void __launch_bounds__(kLeafThreads, 1) leaf_chol_inv_kernel(const __
         smem_gemm<1>(g, cnt);
     }
 
-    // ---- store X (lower, zeros above) and X^T (upper, zeros below) as hi/lo
+    // ---- store X (lower, zeros above) and X^T (upper, zeros below)
     for (int idx = tid; idx < n * n; idx += kLeafThreads) {
         const int r = idx / n, c = idx % n;
-        const float x = (c <= r) ? Xs[r * kLeafPitch + c] : 0.0f;
-        const float hi = ptx::tf32_round(x);
-        const float lo = ptx::tf32_round(x - hi);
-        A.x_hi[(size_t)r * A.ld + c] = hi;
-        A.x_lo[(size_t)r * A.ld + c] = lo;
-        const float xt = (r <= c) ? Xs[c * kLeafPitch + r] : 0.0f;
-        const float thi = ptx::tf32_round(xt);
-        A.xt_hi[(size_t)r * A.ld + c] = thi;
-        A.xt_lo[(size_t)r * A.ld + c] = ptx::tf32_round(xt - thi);
+        A.x[(size_t)r * A.ld + c] = (c <= r) ? Xs[r * kLeafPitch + c] : 0.0f;
+        A.xt[(size_t)r * A.ld + c] = (r <= c) ? Xs[c * kLeafPitch + r] : 0.0f;
     }
     if (tid == 0 && *bad != INT_MAX) {
         // keep the smallest failing column across blocks (0 = success)

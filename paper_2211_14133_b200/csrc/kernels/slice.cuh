@@ -1,0 +1,97 @@
+// Operand preparation for the fp32-accurate int8 tensor-core GEMM (kOZ8):
+// every row of an fp32 matrix is written as
+//     x = 2^e * (q0 2^-7 + q1 2^-14 + q2 2^-21 + q3 2^-28),   q_s in [-127, 127]
+// with one power-of-two scale per row (max|x| in [2^(e-1), 2^e)).  All digit
+// extractions are exact fp32 operations (power-of-two scaling and removal of
+// the integer part), so the only error is the last digit's rounding:
+// |x - x~| <= 2^(e-29) <= 2^-28 max|row|.
+//
+// Layout of a sliced operand (one allocation): 4 int8 planes of rows x kpad
+// bytes (kpad = k rounded up to 16 for TMA row pitch), then rows int32
+// exponents, then rows fp64 squared norms of the REPRESENTED row
+// sum_k x~_k^2 * 2^-2e over the valid range.  The GEMM writes the diagonal of
+// a same-operand product (X X^T) from these: the omitted digit product
+// (q2*q2, weight 2^-42) is >= 0 on the diagonal, so dropping it there would be
+// a bias that grows linearly with k; off the diagonal it is an unbiased
+// 2^-28-level error.  Columns outside a row's valid (block-triangular) range are
+// neither read nor written: the GEMM's k-range never loads them.
+#pragma once
+
+#include <cstdint>
+
+namespace pf {
+
+enum SliceMode : int {
+    SLICE_FULL = 0,
+    SLICE_LOWER_BLOCK = 1,  // row r valid for k < (r/128 + 1) * 128
+    SLICE_UPPER_BLOCK = 2,  // row r valid for k >= (r/128) * 128
+};
+
+struct SliceJob {
+    const float* src;
+    int rows, k, ld;
+    int mode;
+    int8_t* planes;
+    int64_t plane_stride;  // bytes between digit planes
+    int kpad;
+    int* exps;
+    double* sqnorm;
+};
+
+constexpr int kMaxSliceJobs = 32;
+struct SliceBatch {
+    SliceJob j[kMaxSliceJobs];
+};
+
+__device__ __forceinline__ void valid_range(const SliceJob& J, int r, int& lo, int& hi) {
+    lo = 0;
+    hi = J.k;
+    if (J.mode == SLICE_LOWER_BLOCK) hi = min(J.k, (r / 128 + 1) * 128);
+    if (J.mode == SLICE_UPPER_BLOCK) lo = (r / 128) * 128;
+}
+
+// one warp per row; grid (ceil(rows / 8), jobs)
+__global__ void __launch_bounds__(256) slice_kernel(const __grid_constant__ SliceBatch b) {
+    const SliceJob& J = b.j[blockIdx.y];
+    const int r = blockIdx.x * 8 + (threadIdx.x >> 5);
+    const int lane = threadIdx.x & 31;
+    if (r >= J.rows) return;
+    int lo, hi;
+    valid_range(J, r, lo, hi);
+    const float* row = J.src + static_cast<int64_t>(r) * J.ld;
+    float m = 0.0f;
+    for (int c = lo + lane; c < hi; c += 32) m = fmaxf(m, fabsf(row[c]));
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, o));
+    int e = 0;
+    if (m > 0.0f) {
+        int ex;
+        frexpf(m, &ex);  // m = f * 2^ex, f in [0.5, 1)
+        e = ex;          // so max|row| < 2^e
+    }
+    if (lane == 0) J.exps[r] = e;
+    int8_t* p0 = J.planes + static_cast<int64_t>(r) * J.kpad;
+    double sq = 0.0;
+    for (int c = lo + lane; c < hi; c += 32) {
+        float t = ldexpf(row[c], 7 - e);  // x * 2^-e * 2^7, |t| < 128
+        const float q0 = truncf(t);
+        t = (t - q0) * 128.0f;
+        const float q1 = truncf(t);
+        t = (t - q1) * 128.0f;
+        const float q2 = truncf(t);
+        t = (t - q2) * 128.0f;
+        const float q3 = fminf(fmaxf(rintf(t), -127.0f), 127.0f);
+        p0[c] = static_cast<int8_t>(q0);
+        p0[c + J.plane_stride] = static_cast<int8_t>(q1);
+        p0[c + 2 * J.plane_stride] = static_cast<int8_t>(q2);
+        p0[c + 3 * J.plane_stride] = static_cast<int8_t>(q3);
+        const double rep = ldexp(static_cast<double>(q0), -7) + ldexp(static_cast<double>(q1), -14) +
+                           ldexp(static_cast<double>(q2), -21) + ldexp(static_cast<double>(q3), -28);
+        sq = fma(rep, rep, sq);
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) sq += __shfl_xor_sync(0xffffffffu, sq, o);
+    if (lane == 0) J.sqnorm[r] = sq;
+}
+
+}  // namespace pf

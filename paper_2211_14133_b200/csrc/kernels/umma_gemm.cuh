@@ -1,20 +1,28 @@
 // Grouped "TN" tensor-core GEMM for sm_100a: C = alpha * A * B^T (+ beta * C)
 // with A [rows x k] and B [cols x k] both K-major (K contiguous).  One kernel
-// serves every K-FAC hot op:
+// template serves every K-FAC hot op:
 //
-//   * curvature SYRK   A = B = X (bf16 [d x n_tokens]),  lower tiles only,
-//                      mirrored store -> full symmetric fp32 factor;
-//   * damped inverse   trailing updates / triangular products in 3xTF32
-//                      (fp32-accurate: hi*hi + hi*lo + lo*hi);
-//   * precondition     U^T = A^-1 G^T, P = B^-1 U  (3xTF32) with the fused
-//                      weight-update epilogue W -= eta * P.
+//   kFmt = kBF16   curvature SYRK: A = B = X (bf16 [d x n_tokens]), lower tiles
+//                  only, mirrored store -> full symmetric fp32 factor.
+//                  kind::f16, 1 operand plane, fp32 accumulator in TMEM.
+//   kFmt = kOZ8    fp32-accurate products (damped-inverse recursion,
+//                  preconditioning): each fp32 operand row is pre-sliced
+//                  (slice kernel) into a power-of-two row scale 2^e and four
+//                  int8 digits q0..q3 of 7 bits each (x = 2^e sum_s q_s 2^-7(s+1)).
+//                  The 10 digit products with s_a + s_b <= 3 run as
+//                  tcgen05.mma.kind::i8 with EXACT int32 accumulation, one TMEM
+//                  accumulator per digit weight g = s_a + s_b (4 x 128 columns =
+//                  all 512), recombined in fp64 in the epilogue.  Error: 2^-27 of
+//                  the row scale from slicing, none from accumulation — unlike
+//                  the fp32-accumulated tf32 split we measured first, whose
+//                  inverse residual grew linearly with d.
 //
-// Structure (per CTA = one 128x128 output tile, 4 warps):
-//   warp 0 / lane 0 : TMA producer, STAGES-deep smem ring (full/empty mbarriers)
-//   warp 1 / lane 0 : tcgen05.mma issuer, accumulator in TMEM (128 lanes x 128 cols)
+// Structure (one CTA = one 128x128 output tile, 4 warps):
+//   warp 0 / lane 0 : TMA producer, kStages-deep smem ring (full/empty mbarriers)
+//   warp 1 / lane 0 : tcgen05.mma issuer (single thread)
 //   all 4 warps     : epilogue, tcgen05.ld 32x32b -> registers -> global
-// Operand tiles are 128 rows x 128 B, TMA SWIZZLE_128B, so each k-block is
-// 64 bf16 or 32 fp32 elements and is consumed by 4 UMMA k-steps of 32 B.
+// Operand tiles: bf16 128 rows x 128 B (SWIZZLE_128B, 64 elements per k-block);
+// int8 digits 128 rows x 64 B (SWIZZLE_64B, 64 elements per k-block).
 #pragma once
 
 #include <cuda.h>
@@ -24,23 +32,23 @@
 
 namespace pf {
 
-constexpr int kTile = 128;            // output tile edge (M = N = 128)
-constexpr int kTileBytes = 128 * 128; // one operand plane per stage: 128 rows x 128 B
-constexpr int kMaxMaps = 64;
+constexpr int kTile = 128;
+constexpr int kMaxMaps = 96;
 constexpr int kMaxProbs = 16;
+constexpr int kBF16 = 1;
+constexpr int kOZ8 = 3;
+constexpr int kDigits = 4;  // int8 digits per fp32 value (28 bits)
 
 enum EpiFlag : uint32_t {
-    EPI_MIRROR = 1u,        // off-diagonal tiles also stored transposed (symmetric result)
-    EPI_TRANSPOSE = 2u,     // store C^T (into c) instead of C
-    EPI_SPLIT = 4u,         // store hi=tf32(v) to c, lo=tf32(v-hi) to c_lo
-    EPI_READ_SPLIT = 8u,    // old value = c + c_lo (when beta != 0)
-    EPI_ALSO_T = 16u,       // additionally store C^T into c_t (+ c_t_lo if SPLIT)
-    EPI_VEC4 = 32u,         // c / ldc 16-byte aligned: vectorised row stores
+    EPI_MIRROR = 1u,     // off-diagonal tiles also stored transposed (symmetric result)
+    EPI_TRANSPOSE = 2u,  // store C^T (into c) instead of C
+    EPI_ALSO_T = 16u,    // additionally store C^T into c_t
+    EPI_VEC4 = 32u,      // c / ldc 16-byte aligned: vectorised row stores
+    EPI_EXACT_DIAG = 64u,  // kOZ8, A == B: diagonal from the operand's exact row norms
 };
 
-// k_mode: which slice of the reduction a tile needs (triangular operands).
 // Tile (tm, tn) reads only the k-slice where both triangular operands can be
-// non-zero; the rest of the slice is never touched (no zero-fill needed).
+// non-zero; the rest is never touched (no zero-fill needed outside it).
 enum KMode : int {
     K_FULL = 0,
     K_FROM_ROW_TILE = 1,    // k in [tm*128, k)
@@ -50,18 +58,19 @@ enum KMode : int {
 };
 
 struct GemmDesc {
-    int a_map, b_map;    // index of plane 0's CUtensorMap (plane 1 = +1)
-    int rows, cols, k;   // output rows (A rows), output cols (B rows), reduction length
+    int a_map, b_map;   // index of the first plane's CUtensorMap (digit s = +s)
+    int rows, cols, k;
     int tiles_m, tiles_n;
-    int lower;           // enumerate only tiles with tm >= tn
-    int tile_begin;      // first global tile index of this problem
+    int lower;          // enumerate only tiles with tm >= tn
+    int tile_begin;
     int k_mode;
     float alpha, beta;
     uint32_t flags;
+    const int* a_exp;   // kOZ8: per-row scale exponents of A / B
+    const int* b_exp;
+    const double* a_sqnorm;  // kOZ8 + EPI_EXACT_DIAG
     float* c;
-    float* c_lo;
     float* c_t;
-    float* c_t_lo;
     int ldc, ldc_t;
 };
 
@@ -72,12 +81,21 @@ struct GemmBatch {
     int total_tiles;
 };
 
-template <int kFmt, int kPlanes, int kStages>
+template <int kFmt>
 struct GemmTraits {
-    static constexpr int kStageBytes = 2 * kPlanes * kTileBytes;
-    static constexpr int kSmemBytes = kStages * kStageBytes + 1024 /*align*/ + 256 /*barriers*/;
-    static constexpr int kKBlock = kFmt == 1 ? 64 : 32;  // elements per 128-B row
-    static constexpr uint32_t kIdesc = ptx::make_idesc(kFmt, 128, 128);
+    static constexpr int kPlanes = kFmt == kOZ8 ? kDigits : 1;
+    static constexpr int kPlaneBytes = kFmt == kOZ8 ? 128 * 64 : 128 * 128;
+    static constexpr int kStageBytes = 2 * kPlanes * kPlaneBytes;
+    static constexpr int kStages = 3;
+    static constexpr int kSmemBytes = kStages * kStageBytes + 1024 + 256;
+    static constexpr int kKBlock = 64;  // elements per k-block (both formats)
+    static constexpr int kKSteps = kFmt == kOZ8 ? 2 : 4;  // 32-byte UMMA k-steps per block
+    static constexpr uint32_t kTmemCols = kFmt == kOZ8 ? 512 : 128;
+    static constexpr int kMinBlocks = kFmt == kOZ8 ? 1 : 2;
+    // kind::i8: signed int8 A/B (format 1), s32 accumulate (c_format 2)
+    static constexpr uint32_t kIdesc =
+        kFmt == kOZ8 ? ((2u << 4) | (1u << 7) | (1u << 10) | ((128u >> 3) << 17) | ((128u >> 4) << 24))
+                     : ptx::make_idesc(1, 128, 128);
 };
 
 __device__ __forceinline__ void decode_lower(int t, int& tm, int& tn) {
@@ -88,20 +106,11 @@ __device__ __forceinline__ void decode_lower(int t, int& tm, int& tn) {
     tn = t - m * (m + 1) / 2;
 }
 
-__device__ __forceinline__ void put(float* hi, float* lo, size_t idx, float v, bool split) {
-    if (split) {
-        const float h = ptx::tf32_round(v);
-        hi[idx] = h;
-        lo[idx] = ptx::tf32_round(v - h);
-    } else {
-        hi[idx] = v;
-    }
-}
-
-template <int kFmt, int kPlanes, int kStages>
-__global__ void __launch_bounds__(128, (kPlanes == 1 ? 2 : 1))
+template <int kFmt>
+__global__ void __launch_bounds__(128, GemmTraits<kFmt>::kMinBlocks)
     umma_gemm_kernel(const __grid_constant__ GemmBatch batch) {
-    using T = GemmTraits<kFmt, kPlanes, kStages>;
+    using T = GemmTraits<kFmt>;
+    constexpr int kStages = T::kStages;
     extern __shared__ uint8_t smem_raw[];
     uint8_t* smem = reinterpret_cast<uint8_t*>(
         (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~static_cast<uintptr_t>(1023));
@@ -110,7 +119,6 @@ __global__ void __launch_bounds__(128, (kPlanes == 1 ? 2 : 1))
     uint64_t* done = empty + kStages;
     uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(done + 1);
 
-    // ---- which problem / tile
     const int gt = blockIdx.x;
     int p = 0;
     while (p + 1 < batch.n_probs && batch.probs[p + 1].tile_begin <= gt) ++p;
@@ -129,7 +137,7 @@ __global__ void __launch_bounds__(128, (kPlanes == 1 ? 2 : 1))
     if (P.k_mode == K_TO_ROW_TILE_END) k_end = min(P.k, (tm + 1) * kTile);
     if (P.k_mode == K_TO_COL_TILE_END) k_end = min(P.k, (tn + 1) * kTile);
     const int kb0 = k_begin / T::kKBlock;
-    const int kb1 = (k_end + T::kKBlock - 1) / T::kKBlock;
+    const int kb1 = max(kb0, (k_end + T::kKBlock - 1) / T::kKBlock);
 
     const int warp = threadIdx.x >> 5;
     const uint32_t lane = threadIdx.x & 31;
@@ -142,20 +150,20 @@ __global__ void __launch_bounds__(128, (kPlanes == 1 ? 2 : 1))
         ptx::mbar_init(done, 1);
         ptx::fence_barrier_init();
     }
-    if (warp == 0) ptx::tmem_alloc<128>(tmem_slot);
+    if (warp == 0) ptx::tmem_alloc<T::kTmemCols>(tmem_slot);
     ptx::tc_fence_before();
     __syncthreads();
     ptx::tc_fence_after();
     const uint32_t tmem = *tmem_slot;
 
-    auto a_plane = [&](int s, int pl) { return smem + s * T::kStageBytes + pl * kTileBytes; };
+    auto a_plane = [&](int s, int pl) { return smem + s * T::kStageBytes + pl * T::kPlaneBytes; };
     auto b_plane = [&](int s, int pl) {
-        return smem + s * T::kStageBytes + (kPlanes + pl) * kTileBytes;
+        return smem + s * T::kStageBytes + (T::kPlanes + pl) * T::kPlaneBytes;
     };
 
     if (warp == 0 && lane == 0) {
         // ---------------- TMA producer
-        for (int pl = 0; pl < kPlanes; ++pl) {
+        for (int pl = 0; pl < T::kPlanes; ++pl) {
             ptx::prefetch_tmap(&batch.maps[P.a_map + pl]);
             ptx::prefetch_tmap(&batch.maps[P.b_map + pl]);
         }
@@ -165,11 +173,9 @@ __global__ void __launch_bounds__(128, (kPlanes == 1 ? 2 : 1))
             ptx::mbar_wait(&empty[s], ph ^ 1u);
             ptx::mbar_arrive_expect_tx(&full[s], T::kStageBytes);
             const int kc = kb * T::kKBlock;
-            for (int pl = 0; pl < kPlanes; ++pl) {
-                ptx::tma_load_2d(a_plane(s, pl), &batch.maps[P.a_map + pl], &full[s], kc,
-                                 tm * kTile);
-                ptx::tma_load_2d(b_plane(s, pl), &batch.maps[P.b_map + pl], &full[s], kc,
-                                 tn * kTile);
+            for (int pl = 0; pl < T::kPlanes; ++pl) {
+                ptx::tma_load_2d(a_plane(s, pl), &batch.maps[P.a_map + pl], &full[s], kc, tm * kTile);
+                ptx::tma_load_2d(b_plane(s, pl), &batch.maps[P.b_map + pl], &full[s], kc, tn * kTile);
             }
             if (++s == kStages) {
                 s = 0;
@@ -180,30 +186,30 @@ __global__ void __launch_bounds__(128, (kPlanes == 1 ? 2 : 1))
         // ---------------- MMA issuer (single thread)
         int s = 0;
         uint32_t ph = 0;
-        uint32_t acc = 0;
+        uint32_t started = 0;  // bit g: accumulator g has been initialised
         for (int kb = kb0; kb < kb1; ++kb) {
             ptx::mbar_wait(&full[s], ph);
             ptx::tc_fence_after();
-            const uint32_t a0 = ptx::smem_u32(a_plane(s, 0));
-            const uint32_t b0 = ptx::smem_u32(b_plane(s, 0));
 #pragma unroll
-            for (int ks = 0; ks < 4; ++ks) {
+            for (int ks = 0; ks < T::kKSteps; ++ks) {
                 const uint32_t off = ks * 32;  // 32 B per UMMA k-step
-                if constexpr (kPlanes == 1) {
-                    ptx::umma_f16(tmem, ptx::sw128_kmajor_desc(a0 + off),
-                                  ptx::sw128_kmajor_desc(b0 + off), T::kIdesc, acc);
-                    acc = 1;
+                if constexpr (kFmt == kOZ8) {
+#pragma unroll
+                    for (int g = 0; g < kDigits; ++g) {
+#pragma unroll
+                        for (int sa = 0; sa <= g; ++sa) {
+                            const int sb = g - sa;
+                            const uint64_t da = ptx::sw64_kmajor_desc(ptx::smem_u32(a_plane(s, sa)) + off);
+                            const uint64_t db = ptx::sw64_kmajor_desc(ptx::smem_u32(b_plane(s, sb)) + off);
+                            ptx::umma_i8(tmem + g * 128, da, db, T::kIdesc, (started >> g) & 1u);
+                            started |= 1u << g;
+                        }
+                    }
                 } else {
-                    const uint32_t a1 = a0 + kTileBytes;
-                    const uint32_t b1 = b0 + kTileBytes;
-                    // small cross terms first, then the dominant hi*hi product
-                    ptx::umma_tf32(tmem, ptx::sw128_kmajor_desc(a0 + off),
-                                   ptx::sw128_kmajor_desc(b1 + off), T::kIdesc, acc);
-                    acc = 1;
-                    ptx::umma_tf32(tmem, ptx::sw128_kmajor_desc(a1 + off),
-                                   ptx::sw128_kmajor_desc(b0 + off), T::kIdesc, acc);
-                    ptx::umma_tf32(tmem, ptx::sw128_kmajor_desc(a0 + off),
-                                   ptx::sw128_kmajor_desc(b0 + off), T::kIdesc, acc);
+                    ptx::umma_f16(tmem, ptx::sw128_kmajor_desc(ptx::smem_u32(a_plane(s, 0)) + off),
+                                  ptx::sw128_kmajor_desc(ptx::smem_u32(b_plane(s, 0)) + off),
+                                  T::kIdesc, started);
+                    started = 1;
                 }
             }
             ptx::umma_commit(&empty[s]);  // slot free once these MMAs retire
@@ -227,37 +233,64 @@ __global__ void __launch_bounds__(128, (kPlanes == 1 ? 2 : 1))
     const bool row_ok = r < P.rows;
     const uint32_t f = P.flags;
     const bool mirror = (f & EPI_MIRROR) && tm != tn;
+    const uint32_t lane_base = tmem + (static_cast<uint32_t>(warp * 32) << 16);
+    double row_scale = 1.0;
+    if constexpr (kFmt == kOZ8) {
+        if (row_ok) row_scale = ldexp(1.0, P.a_exp[r]);
+    }
 #pragma unroll 1
     for (int chunk = 0; chunk < kTile / 16; ++chunk) {
         __syncwarp();  // tcgen05.ld is .sync.aligned: re-converge first
-        float v[16];
-        if (have_acc) {
-            ptx::tmem_ld16(tmem + (static_cast<uint32_t>(warp * 32) << 16) + chunk * 16, v);
-        } else {
-#pragma unroll
-            for (int j = 0; j < 16; ++j) v[j] = 0.0f;
-        }
         const int c0 = tn * kTile + chunk * 16;
-        if (!row_ok || c0 >= P.cols) continue;
         float out[16];
+        if constexpr (kFmt == kOZ8) {
+            // accumulator g counts units of 2^-7(g+2) of 2^(e_a + e_b)
+            double sum[16];
 #pragma unroll
-        for (int j = 0; j < 16; ++j) out[j] = P.alpha * v[j];
+            for (int j = 0; j < 16; ++j) sum[j] = 0.0;
+            if (have_acc) {
+#pragma unroll
+                for (int g = kDigits - 1; g >= 0; --g) {
+                    float raw[16];
+                    ptx::tmem_ld16(lane_base + g * 128 + chunk * 16, raw);
+                    const double w = ldexp(1.0, -7 * (g + 2));
+#pragma unroll
+                    for (int j = 0; j < 16; ++j)
+                        sum[j] = fma(static_cast<double>(__float_as_int(raw[j])), w, sum[j]);
+                }
+            }
+            if ((f & EPI_EXACT_DIAG) && tm == tn && row_ok && r >= c0 && r < c0 + 16)
+                sum[r - c0] = P.a_sqnorm[r];  // exact sum of squares of the represented row
+#pragma unroll
+            for (int j = 0; j < 16; ++j) {
+                const int c = c0 + j;
+                const double cs = (row_ok && c < P.cols) ? ldexp(row_scale, P.b_exp[c]) : 0.0;
+                out[j] = static_cast<float>(static_cast<double>(P.alpha) * (sum[j] * cs));
+            }
+        } else {
+            float v[16];
+            if (have_acc) {
+                ptx::tmem_ld16(lane_base + chunk * 16, v);
+            } else {
+#pragma unroll
+                for (int j = 0; j < 16; ++j) v[j] = 0.0f;
+            }
+#pragma unroll
+            for (int j = 0; j < 16; ++j) out[j] = P.alpha * v[j];
+        }
+        if (!row_ok || c0 >= P.cols) continue;
         if (P.beta != 0.0f) {
-            // old value from the (row-major or transposed) destination
 #pragma unroll
             for (int j = 0; j < 16; ++j) {
                 const int c = c0 + j;
                 if (c >= P.cols) break;
                 const size_t idx = (f & EPI_TRANSPOSE) ? static_cast<size_t>(c) * P.ldc + r
                                                        : static_cast<size_t>(r) * P.ldc + c;
-                float old = P.c[idx];
-                if (f & EPI_READ_SPLIT) old += P.c_lo[idx];
-                out[j] += P.beta * old;
+                out[j] = fmaf(P.beta, P.c[idx], out[j]);
             }
         }
         const bool full_chunk = c0 + 16 <= P.cols;
-        const bool split = (f & EPI_SPLIT) != 0;
-        if ((f & EPI_VEC4) && full_chunk && !(f & (EPI_TRANSPOSE | EPI_SPLIT))) {
+        if ((f & EPI_VEC4) && full_chunk && !(f & EPI_TRANSPOSE)) {
             float4* dst = reinterpret_cast<float4*>(P.c + static_cast<size_t>(r) * P.ldc + c0);
 #pragma unroll
             for (int q = 0; q < 4; ++q)
@@ -266,31 +299,27 @@ __global__ void __launch_bounds__(128, (kPlanes == 1 ? 2 : 1))
             // lanes hold consecutive rows -> each transposed column store is coalesced
 #pragma unroll
             for (int j = 0; j < 16; ++j)
-                if (c0 + j < P.cols)
-                    put(P.c, P.c_lo, static_cast<size_t>(c0 + j) * P.ldc + r, out[j], split);
+                if (c0 + j < P.cols) P.c[static_cast<size_t>(c0 + j) * P.ldc + r] = out[j];
         } else {
 #pragma unroll
             for (int j = 0; j < 16; ++j)
-                if (c0 + j < P.cols)
-                    put(P.c, P.c_lo, static_cast<size_t>(r) * P.ldc + c0 + j, out[j], split);
+                if (c0 + j < P.cols) P.c[static_cast<size_t>(r) * P.ldc + c0 + j] = out[j];
         }
         if (mirror) {
 #pragma unroll
             for (int j = 0; j < 16; ++j)
-                if (c0 + j < P.cols)
-                    put(P.c, P.c_lo, static_cast<size_t>(c0 + j) * P.ldc + r, out[j], split);
+                if (c0 + j < P.cols) P.c[static_cast<size_t>(c0 + j) * P.ldc + r] = out[j];
         }
         if (f & EPI_ALSO_T) {
 #pragma unroll
             for (int j = 0; j < 16; ++j)
-                if (c0 + j < P.cols)
-                    put(P.c_t, P.c_t_lo, static_cast<size_t>(c0 + j) * P.ldc_t + r, out[j], split);
+                if (c0 + j < P.cols) P.c_t[static_cast<size_t>(c0 + j) * P.ldc_t + r] = out[j];
         }
     }
 
     ptx::tc_fence_before();
     __syncthreads();
-    if (warp == 0) ptx::tmem_dealloc<128>(tmem);
+    if (warp == 0) ptx::tmem_dealloc<T::kTmemCols>(tmem);
 }
 
 }  // namespace pf

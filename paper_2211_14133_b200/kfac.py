@@ -1,0 +1,346 @@
+"""Python mirror of the reference K-FAC API (``pipefill::kfac`` in
+/root/reference/proj/include/pipefill/kfac/{kfac,matrix}.hpp) running on the
+B200 kernels through the C-ABI (include/pf_kfac.h).
+
+Tensors are CUDA torch tensors (torch is plumbing: allocation and streams).
+Layout follows the reference: a BatchTape holds a_l (d_in x batch) and e_l
+(d_out x batch) with examples as columns — on the device in bf16, which is
+exactly the K-major operand the tcgen05 SYRK consumes.  Factors, inverses,
+gradients and weights are fp32, row-major.
+
+Errors follow the reference: shape mismatches raise ``ValueError``
+(std::invalid_argument), a failed Cholesky pivot raises
+:class:`NotPositiveDefinite` (std::domain_error), raised after the stream
+is synchronised.
+"""
+from __future__ import annotations
+
+import ctypes as C
+from dataclasses import dataclass, field
+from typing import Dict, List, Optional, Sequence, Tuple
+
+import torch
+
+from . import _lib as L
+
+
+class NotPositiveDefinite(ArithmeticError):
+    """std::domain_error("cholesky: matrix not positive definite")."""
+
+    def __init__(self, column: int):
+        super().__init__(f"cholesky: matrix not positive definite (damping too small?) "
+                         f"at column {column}")
+        self.column = column
+
+
+def _require_device(t: torch.Tensor, what: str):
+    if not t.is_cuda:
+        raise ValueError(f"{what}: expected a CUDA tensor (no CPU path exists)")
+
+
+def _stream() -> int:
+    return torch.cuda.current_stream().cuda_stream
+
+
+def _ptr(t: Optional[torch.Tensor]) -> Optional[int]:
+    return None if t is None else t.data_ptr()
+
+
+def device_ok() -> bool:
+    return bool(L.lib().pf_device_ok())
+
+
+def kernel_launches() -> int:
+    """Kernels launched by libpf_b200.so since load (host-side counter)."""
+    return int(L.lib().pf_kernel_launch_count())
+
+
+class _Workspaces:
+    """Per-device scratch arena: grows, never shrinks; hot calls allocate nothing."""
+
+    def __init__(self):
+        self._bufs: Dict[Tuple[int, str], torch.Tensor] = {}
+
+    def get(self, nbytes: int, device: torch.device, tag: str = "ws") -> torch.Tensor:
+        key = (device.index or 0, tag)
+        buf = self._bufs.get(key)
+        if buf is None or buf.numel() < nbytes:
+            buf = torch.empty(max(nbytes, 256), dtype=torch.uint8, device=device)
+            self._bufs[key] = buf
+        return buf
+
+
+_WS = _Workspaces()
+
+
+def to_tape_layout(x: torch.Tensor) -> torch.Tensor:
+    """bf16, contiguous, column count padded to a multiple of 8 (16-byte rows
+    for TMA); zero columns do not change X X^T."""
+    _require_device(x, "tape")
+    if x.dim() != 2:
+        raise ValueError("tape matrices are 2-D (features x examples)")
+    d, n = x.shape
+    n8 = (n + 7) // 8 * 8
+    if x.dtype == torch.bfloat16 and x.is_contiguous() and n8 == n:
+        return x
+    out = torch.zeros((d, n8), dtype=torch.bfloat16, device=x.device)
+    out[:, :n] = x
+    return out
+
+
+# ------------------------------------------------------------------ curvature
+def syrk(problems: Sequence[Tuple[torch.Tensor, torch.Tensor, float, bool]],
+         fill_upper: bool = True) -> None:
+    """Grouped F = scale * X X^T (+F).  problems: (x_bf16 [d x n], f_fp32 [d x d], scale, accumulate)."""
+    arr = (L.PfSyrkProblem * len(problems))()
+    for i, (x, f, scale, acc) in enumerate(problems):
+        _require_device(x, "syrk x")
+        _require_device(f, "syrk f")
+        if x.dtype != torch.bfloat16 or f.dtype != torch.float32:
+            raise ValueError("syrk: x must be bf16 and f fp32")
+        if f.shape != (x.shape[0], x.shape[0]) or f.stride(1) != 1 or x.stride(1) != 1:
+            raise ValueError("syrk: shape mismatch")
+        arr[i] = L.PfSyrkProblem(x.data_ptr(), f.data_ptr(), x.shape[0], x.shape[1], x.stride(0),
+                                 f.stride(0), float(scale), int(bool(acc)))
+    L.check(L.lib().pf_curvature_syrk_grouped(arr, len(problems), int(fill_upper), _stream()),
+            "curvature_syrk")
+
+
+@dataclass
+class BatchTape:  # kfac.hpp:33-37
+    layer_inputs: List[torch.Tensor] = field(default_factory=list)   # a_l: d_in x batch
+    layer_errors: List[torch.Tensor] = field(default_factory=list)   # e_l: d_out x batch
+    batch_size: int = 0
+
+
+def curvature_factors(tape: BatchTape, layer: int) -> Tuple[torch.Tensor, torch.Tensor]:
+    """A = (1/bs) a a^T, B = (1/bs) e e^T (kfac.cpp:125-131), one grouped launch."""
+    a = to_tape_layout(tape.layer_inputs[layer])
+    e = to_tape_layout(tape.layer_errors[layer])
+    if tape.batch_size < 1:
+        raise ValueError("batch is empty")
+    A = torch.empty((a.shape[0], a.shape[0]), dtype=torch.float32, device=a.device)
+    B = torch.empty((e.shape[0], e.shape[0]), dtype=torch.float32, device=e.device)
+    inv_b = 1.0 / tape.batch_size
+    syrk([(a, A, inv_b, False), (e, B, inv_b, False)])
+    return A, B
+
+
+# ------------------------------------------------------------------ inverse
+def inverse_workspace_bytes(d: int) -> int:
+    n = C.c_size_t()
+    L.check(L.lib().pf_damped_inverse_workspace(d, n), "inverse workspace")
+    return n.value
+
+
+def slice_bytes(rows: int, k: int) -> int:
+    n = C.c_size_t()
+    L.check(L.lib().pf_slice_bytes(rows, k, n), "slice bytes")
+    return n.value
+
+
+@dataclass
+class SlicedMatrix:
+    """Digit form of an fp32 matrix (pf_slice): what the tensor-core
+    preconditioner consumes.  ``fp32`` keeps the plain inverse."""
+    fp32: torch.Tensor
+    digits: torch.Tensor  # uint8 buffer of slice_bytes(rows, k)
+
+
+def slice_matrix(x: torch.Tensor) -> SlicedMatrix:
+    _require_device(x, "slice")
+    if x.dtype != torch.float32 or x.stride(1) != 1:
+        raise ValueError("slice: expects row-major fp32")
+    buf = torch.empty(slice_bytes(x.shape[0], x.shape[1]), dtype=torch.uint8, device=x.device)
+    L.check(L.lib().pf_slice(x.data_ptr(), x.shape[0], x.shape[1], x.stride(0), buf.data_ptr(),
+                             _stream()), "slice")
+    return SlicedMatrix(x, buf)
+
+
+def damped_inverse_batched(mats: Sequence[torch.Tensor], damping: float,
+                           outs: Optional[Sequence[torch.Tensor]] = None,
+                           digits: Optional[Sequence[torch.Tensor]] = None,
+                           check: bool = True) -> List[torch.Tensor]:
+    """(M_i + damping I)^-1 for every M_i in one batched launch sequence.
+    With ``digits`` (uint8 buffers of slice_bytes(d, d)) the digit form of each
+    inverse is written as well."""
+    if not mats:
+        return []
+    dev = mats[0].device
+    sizes = [inverse_workspace_bytes(m.shape[0]) for m in mats]
+    offs, total = [], 0
+    for s in sizes:
+        offs.append(total)
+        total += (s + 255) // 256 * 256
+    ws = _WS.get(total, dev, "inverse")
+    info = _WS.get(4 * len(mats), dev, "info").view(torch.int32)[: len(mats)]
+    outs = list(outs) if outs is not None else [torch.empty_like(m, dtype=torch.float32) for m in mats]
+    arr = (L.PfInverseProblem * len(mats))()
+    for i, m in enumerate(mats):
+        _require_device(m, "cholesky_spd_inverse")
+        if m.dim() != 2 or m.shape[0] != m.shape[1]:
+            raise ValueError("cholesky_spd_inverse: matrix not square")
+        if m.dtype != torch.float32 or m.stride(1) != 1:
+            raise ValueError("cholesky_spd_inverse: expects row-major fp32")
+        dg = None if digits is None else digits[i]
+        arr[i] = L.PfInverseProblem(m.data_ptr(), outs[i].data_ptr(), _ptr(dg), m.shape[0],
+                                    m.stride(0), outs[i].stride(0), float(damping),
+                                    ws.data_ptr() + offs[i], info[i:].data_ptr())
+    L.check(L.lib().pf_damped_inverse_batched(arr, len(mats), _stream()), "damped_inverse")
+    if check:
+        bad = info.cpu()
+        for i in range(len(mats)):
+            if int(bad[i]) != 0:
+                raise NotPositiveDefinite(int(bad[i]))
+    return outs
+
+
+def cholesky_spd_inverse(m: torch.Tensor, damping: float) -> torch.Tensor:
+    """matrix.hpp:58 — (M + damping I)^-1 via Cholesky (fp32-accurate)."""
+    return damped_inverse_batched([m], damping)[0]
+
+
+# ------------------------------------------------------------------ precondition
+def precondition_workspace_bytes(d_out: int, d_in: int) -> int:
+    n = C.c_size_t()
+    L.check(L.lib().pf_precondition_workspace(d_out, d_in, n), "precondition workspace")
+    return n.value
+
+
+def _check_prec(grad, a_inv, b_inv):
+    for t, n in ((grad, "grad"), (a_inv, "a_inv"), (b_inv, "b_inv")):
+        _require_device(t, n)
+        if t.dtype != torch.float32 or not t.is_contiguous():
+            raise ValueError(f"precondition: {n} must be contiguous fp32")
+    if b_inv.shape[1] != grad.shape[0] or grad.shape[1] != a_inv.shape[0]:
+        raise ValueError("precondition: shape mismatch")
+
+
+def precondition(grad: torch.Tensor, a_inv: torch.Tensor, b_inv: torch.Tensor) -> torch.Tensor:
+    """kfac.hpp:51 — B^-1 G A^-1 (two chained 3xTF32 tensor-core GEMMs)."""
+    _check_prec(grad, a_inv, b_inv)
+    d_out, d_in = grad.shape
+    out = torch.empty_like(grad)
+    nb = precondition_workspace_bytes(d_out, d_in)
+    ws = _WS.get(nb, grad.device, "prec")
+    L.check(L.lib().pf_precondition(b_inv.data_ptr(), grad.data_ptr(), a_inv.data_ptr(),
+                                    out.data_ptr(), d_out, d_in, ws.data_ptr(), nb, _stream()),
+            "precondition")
+    return out
+
+
+def precondition_update(weight: torch.Tensor, grad: torch.Tensor, a_inv: torch.Tensor,
+                        b_inv: torch.Tensor, eta: float) -> None:
+    """W -= eta * B^-1 G A^-1, update fused into the second GEMM's epilogue."""
+    _check_prec(grad, a_inv, b_inv)
+    if weight.shape != grad.shape or not weight.is_contiguous() or weight.dtype != torch.float32:
+        raise ValueError("precondition_update: weight shape mismatch")
+    d_out, d_in = grad.shape
+    nb = precondition_workspace_bytes(d_out, d_in)
+    ws = _WS.get(nb, grad.device, "prec")
+    L.check(L.lib().pf_precondition_update(b_inv.data_ptr(), grad.data_ptr(), a_inv.data_ptr(),
+                                           weight.data_ptr(), d_out, d_in, float(eta),
+                                           ws.data_ptr(), nb, _stream()),
+            "precondition_update")
+
+
+def precondition_update_sliced(items: Sequence[Tuple[Optional[torch.Tensor], torch.Tensor,
+                                                     SlicedMatrix, SlicedMatrix, float]],
+                               p_out: Optional[Sequence[torch.Tensor]] = None) -> None:
+    """Grouped W_i -= eta_i B_i^-1 G_i A_i^-1 with inverses in digit form.
+    items: (weight or None, grad, a_inv, b_inv, eta); p_out receives P instead."""
+    if not items:
+        return
+    dev = items[0][1].device
+    sizes = [precondition_workspace_bytes(g.shape[0], g.shape[1]) for _, g, _, _, _ in items]
+    offs, total = [], 0
+    for s in sizes:
+        offs.append(total)
+        total += (s + 255) // 256 * 256
+    ws = _WS.get(total, dev, "prec_sliced")
+    arr = (L.PfPreconditionProblem * len(items))()
+    for i, (w, g, ai, bi, eta) in enumerate(items):
+        d_out, d_in = g.shape
+        if ai.fp32.shape[0] != d_in or bi.fp32.shape[0] != d_out:
+            raise ValueError("precondition: shape mismatch")
+        arr[i] = L.PfPreconditionProblem(bi.digits.data_ptr(), g.data_ptr(), ai.digits.data_ptr(),
+                                         _ptr(w), None if p_out is None else p_out[i].data_ptr(),
+                                         d_out, d_in, float(eta), ws.data_ptr() + offs[i])
+    L.check(L.lib().pf_precondition_update_sliced(arr, len(items), _stream()),
+            "precondition_update_sliced")
+
+
+# ------------------------------------------------------------------ state / step
+class KfacState:
+    """kfac.hpp:60-73: per-layer factors, damped inverses (fp32 + digit form), staleness."""
+
+    def __init__(self, layers: int = 0, damping: float = 0.0, learning_rate: float = 0.0):
+        self.factor_a: List[Optional[torch.Tensor]] = [None] * layers
+        self.factor_b: List[Optional[torch.Tensor]] = [None] * layers
+        self.inv_a: List[Optional[SlicedMatrix]] = [None] * layers
+        self.inv_b: List[Optional[SlicedMatrix]] = [None] * layers
+        self.staleness = [0] * layers
+        self.refreshed_this_step = [False] * layers
+        self.damping = damping
+        self.learning_rate = learning_rate
+
+    def has_inverses(self, layer: int) -> bool:
+        return self.inv_a[layer] is not None and self.inv_b[layer] is not None
+
+    def update_factors(self, tape: BatchTape) -> None:
+        """Overwrites the factors (no EMA), all layers in one grouped launch."""
+        probs = []
+        inv_b = 1.0 / tape.batch_size
+        for l in range(len(self.factor_a)):
+            a = to_tape_layout(tape.layer_inputs[l])
+            e = to_tape_layout(tape.layer_errors[l])
+            if self.factor_a[l] is None or self.factor_a[l].shape[0] != a.shape[0]:
+                self.factor_a[l] = torch.empty((a.shape[0],) * 2, dtype=torch.float32, device=a.device)
+            if self.factor_b[l] is None or self.factor_b[l].shape[0] != e.shape[0]:
+                self.factor_b[l] = torch.empty((e.shape[0],) * 2, dtype=torch.float32, device=e.device)
+            probs += [(a, self.factor_a[l], inv_b, False), (e, self.factor_b[l], inv_b, False)]
+        syrk(probs, fill_upper=False)  # inversion reads the lower triangle only
+
+    def refresh_inverses(self) -> None:
+        """Invert every layer's damped factors (batched); resets staleness."""
+        mats, slots = [], []
+        for l in range(len(self.factor_a)):
+            if self.factor_a[l] is None:
+                continue
+            mats += [self.factor_a[l], self.factor_b[l]]
+            slots += [(l, 0), (l, 1)]
+        if not mats:
+            return
+        outs = [torch.empty_like(m) for m in mats]
+        digits = [torch.empty(slice_bytes(m.shape[0], m.shape[0]), dtype=torch.uint8,
+                              device=m.device) for m in mats]
+        damped_inverse_batched(mats, self.damping, outs, digits)
+        for (l, which), o, dg in zip(slots, outs, digits):
+            (self.inv_a if which == 0 else self.inv_b)[l] = SlicedMatrix(o, dg)
+            self.staleness[l] = 0
+            self.refreshed_this_step[l] = True
+
+
+@dataclass
+class NgdStepResult:
+    used_plain_gradient: bool = False
+
+
+def ngd_step(weights: List[torch.Tensor], state: KfacState,
+             gradients: List[torch.Tensor]) -> NgdStepResult:
+    """kfac.cpp:186-201: theta_l -= eta * B^-1 G_l A^-1 (grouped, fused update);
+    layers without inverses take the plain gradient and set the flag."""
+    if len(gradients) != len(weights):
+        raise ValueError("one gradient per layer required")
+    out = NgdStepResult()
+    items = []
+    for l, (w, g) in enumerate(zip(weights, gradients)):
+        if state.has_inverses(l):
+            items.append((w, g, state.inv_a[l], state.inv_b[l], state.learning_rate))
+        else:
+            out.used_plain_gradient = True
+            w.sub_(g * state.learning_rate)
+        state.staleness[l] = (0 if state.refreshed_this_step[l] else state.staleness[l]) + 1
+        state.refreshed_this_step[l] = False
+    precondition_update_sliced(items)
+    return out
