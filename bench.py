@@ -8,7 +8,7 @@ unit of the Chimera/1F1B configs the metric is quoted on:
   * curvature: 12 Kronecker factors (A and B of Q, K, V, O, FFN1, FFN2;
     10 x 1024^2 + 2 x 4096^2) from bf16 tapes, one grouped tcgen05 SYRK launch;
   * inversion: 12 damped inverses (lambda = 0.1), fp32-accurate, batched;
-  * precondition: 6 x  W -= eta B^-1 G A^-1  (3xTF32 tcgen05, fused update).
+  * precondition: 6 x  W -= eta B^-1 G A^-1  (fp32-accurate int8-digit tcgen05 GEMMs, fused update).
 Algorithmic FLOPs per step: SYRK d(d+1)n, inverse d^3,
 precondition 2 d_out^2 d_in + 2 d_out d_in^2.  value = those FLOPs / step time.
 
@@ -251,8 +251,26 @@ def run_gpu_arm(args, rank, world, local_rank):
         step()
     torch.cuda.synchronize()
 
+    # One layer step = ~400 small launches (the inversion recursion): the
+    # single-GPU step is captured once as a CUDA graph and replayed, so host
+    # enqueue cost never shows up as GPU idle time.  (N > 1 interleaves NCCL
+    # calls and runs eagerly.)
+    run = step
+    graphed = False
+    if world == 1 and not args.no_graph:
+        launches_per_step = K.kernel_launches()
+        step()
+        torch.cuda.synchronize()
+        launches_per_step = K.kernel_launches() - launches_per_step
+        graph = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(graph):
+            step()
+        graph.replay()
+        torch.cuda.synchronize()
+        run = graph.replay
+        graphed = True
+
     # ---------------------------------------------------------- device timing
-    evs = [[torch.cuda.Event(enable_timing=True) for _ in range(4)] for _ in range(args.steps)]
     if dist: dist.barrier()
     torch.cuda.synchronize()
     launches0 = K.kernel_launches()
@@ -261,12 +279,20 @@ def run_gpu_arm(args, rank, world, local_rank):
         t_end = torch.cuda.Event(enable_timing=True)
         t_start.record(stream)
         for i in range(args.steps):
-            step(evs[i])
+            run()
         t_end.record(stream)
         torch.cuda.synchronize()
     launches = K.kernel_launches() - launches0
+    if graphed:
+        launches = launches_per_step * args.steps  # replays do not pass through the host counter
     if dist: dist.barrier()
     ms = t_start.elapsed_time(t_end) / args.steps
+
+    # phase breakdown: a separate eager pass with events between the phases
+    evs = [[torch.cuda.Event(enable_timing=True) for _ in range(4)] for _ in range(args.steps)]
+    for i in range(args.steps):
+        step(evs[i])
+    torch.cuda.synchronize()
     phases = {"curvature": 0.0, "inversion": 0.0, "precondition": 0.0}
     for e in evs:
         phases["curvature"] += e[0].elapsed_time(e[1]) / args.steps
@@ -351,13 +377,14 @@ def run_gpu_arm(args, rank, world, local_rank):
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "weak",
-        "vs_baseline": None, "dtype": "bf16 curvature / fp32 (3xTF32) inversion+precondition",
+        "vs_baseline": None, "dtype": "bf16 curvature / fp32-accurate (int8-digit tcgen05) inversion+precondition",
         "data": "synthetic (torch.randn tapes/grads/weights, random init)",
         "config": {"workload": "bert_large_kfac_layer_step", "d_model": D_MODEL, "d_ff": D_FF,
                    "tokens_per_micro_batch": TOKENS, "factors": 12, "linears": 6,
                    "damping": DAMPING, "parallelism": f"dp{world}" + ("+inv-parallel" if world > 1 else ""),
                    "l2": "inputs larger than L2 (tapes 144 MB + factors 168 MB per step)"},
         "phases": phase_rates,
+        "cuda_graph": graphed,
         "roofline": roof,
         "e2e": {"value": e2e_value, "unit": UNIT, "ms_per_step": e2e_ms,
                 "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h},
@@ -376,6 +403,7 @@ def main():
     p.add_argument("--warmup", type=int, default=3)
     p.add_argument("--impl", default="ours", choices=["ours", "reference"])
     p.add_argument("--no-cpu-baseline", action="store_true")
+    p.add_argument("--no-graph", action="store_true", help="eager launches instead of a CUDA graph")
     args = p.parse_args()
     rank = int(os.environ.get("RANK", "0"))
     world = int(os.environ.get("WORLD_SIZE", str(args.gpus)))

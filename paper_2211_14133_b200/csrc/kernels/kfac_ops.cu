@@ -222,6 +222,7 @@ void gemm_oz8(const std::vector<GemmSpec>& s, cudaStream_t st) { launch_gemms<kO
 struct Damp2D {
     const float* src;
     float* dst;
+    int* info;  // reset to 0 (success) before the factorisation
     int d, ld_src, ld_dst;
     float damping;
 };
@@ -233,6 +234,7 @@ struct DampBatch {
 // dst = M + damping * I  (lower triangle incl. diagonal; the rest never read)
 __global__ void damp_kernel(const __grid_constant__ DampBatch b) {
     const Damp2D& s = b.e[blockIdx.y];
+    if (blockIdx.x == 0 && threadIdx.x == 0) *s.info = 0;
     const int64_t total = static_cast<int64_t>(s.d) * s.d;
     for (int64_t idx = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; idx < total;
          idx += static_cast<int64_t>(gridDim.x) * blockDim.x) {
@@ -338,6 +340,7 @@ void inverse_rec(const std::vector<InvWs>& ws, int o, int n, cudaStream_t st) {
         s.cols = n1;
         s.k = n1;
         s.k_mode = K_TO_COL_TILE_END;
+        s.flags = EPI_VEC4;
         s.c = at(w.l, w.ld, o + n1, o);
         s.ldc = w.ld;
         g.push_back(s);
@@ -357,6 +360,7 @@ void inverse_rec(const std::vector<InvWs>& ws, int o, int n, cudaStream_t st) {
         s.lower = true;
         s.alpha = -1.0f;
         s.beta = 1.0f;
+        s.flags = EPI_VEC4;
         s.c = at(w.a, w.ld, o + n1, o + n1);
         s.ldc = w.ld;
         g.push_back(s);
@@ -400,7 +404,7 @@ void inverse_rec(const std::vector<InvWs>& ws, int o, int n, cudaStream_t st) {
         s.k = n2;
         s.k_mode = K_TO_ROW_TILE_END;
         s.alpha = -1.0f;
-        s.flags = EPI_ALSO_T;
+        s.flags = EPI_ALSO_T | EPI_VEC4;
         s.c = at(w.x, w.ld, o + n1, o);
         s.ldc = w.ld;
         s.c_t = at(w.xt, w.ld, o, o + n1);
@@ -419,8 +423,7 @@ void damped_inverse_group(const std::vector<const pf_inverse_problem*>& probs, c
         const pf_inverse_problem* p = probs[i];
         InvWs w = carve(p->workspace, d);
         w.info = p->d_info;
-        check(cudaMemsetAsync(p->d_info, 0, sizeof(int), st), "memset(info)");
-        db.e[i] = Damp2D{p->m, w.a, d, p->ldm, w.ld, p->damping};
+        db.e[i] = Damp2D{p->m, w.a, p->d_info, d, p->ldm, w.ld, p->damping};
         ws.push_back(w);
     }
     const int blocks = std::min((d * d + 255) / 256, 148 * 8);
@@ -548,6 +551,53 @@ void precondition_group(const std::vector<PrecJob>& jobs, cudaStream_t st) {
     gemm_oz8(g2, st);
 }
 
+// ------------------------------------------------------------ fork / join
+// Per-thread, per-device pool of non-blocking side streams and events.  A
+// call forks onto them with an event recorded on the caller's stream and
+// joins back with one event per side stream: stream-ordered semantics are
+// kept and the pattern is legal inside CUDA-graph capture.
+struct SidePool {
+    std::vector<cudaStream_t> streams;
+    std::vector<cudaEvent_t> events;  // [0] fork, [1..] joins
+};
+
+SidePool& side_pool(std::size_t n) {
+    thread_local std::vector<SidePool> pools;
+    int dev = 0;
+    check(cudaGetDevice(&dev), "cudaGetDevice");
+    if (pools.size() <= static_cast<std::size_t>(dev)) pools.resize(dev + 1);
+    SidePool& p = pools[dev];
+    while (p.streams.size() < n) {
+        cudaStream_t s;
+        check(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking), "cudaStreamCreate");
+        p.streams.push_back(s);
+    }
+    while (p.events.size() < n + 1) {
+        cudaEvent_t e;
+        check(cudaEventCreateWithFlags(&e, cudaEventDisableTiming), "cudaEventCreate");
+        p.events.push_back(e);
+    }
+    return p;
+}
+
+template <class F>
+void run_forked(std::size_t n, cudaStream_t st, F&& body) {
+    if (n == 0) return;
+    if (n == 1) {
+        body(0, st);
+        return;
+    }
+    SidePool& p = side_pool(n - 1);
+    check(cudaEventRecord(p.events[0], st), "cudaEventRecord(fork)");
+    for (std::size_t g = 1; g < n; ++g) check(cudaStreamWaitEvent(p.streams[g - 1], p.events[0], 0), "fork");
+    body(0, st);
+    for (std::size_t g = 1; g < n; ++g) {
+        body(g, p.streams[g - 1]);
+        check(cudaEventRecord(p.events[g], p.streams[g - 1]), "cudaEventRecord(join)");
+        check(cudaStreamWaitEvent(st, p.events[g], 0), "join");
+    }
+}
+
 }  // namespace
 }  // namespace pf
 
@@ -642,14 +692,22 @@ int pf_damped_inverse_batched(const pf_inverse_problem* problems, int count, voi
                 throw std::invalid_argument("sliced output must be 16-B aligned");
             order.push_back(&p);
         }
-        std::stable_sort(order.begin(), order.end(), [](auto* a, auto* b) { return a->d < b->d; });
-        const cudaStream_t st = static_cast<cudaStream_t>(stream);
+        // Largest first; equal-d problems share every launch (groups of <= 8,
+        // split evenly).  Independent groups run concurrently: the first on
+        // `stream`, the others on side streams forked/joined with events, so
+        // the short d=1024 chains hide under a d=4096 chain.
+        std::stable_sort(order.begin(), order.end(), [](auto* a, auto* b) { return a->d > b->d; });
+        std::vector<std::vector<const pf_inverse_problem*>> groups;
         for (std::size_t i = 0; i < order.size();) {
             std::size_t j = i;
-            while (j < order.size() && order[j]->d == order[i]->d && j - i < 8) ++j;
-            damped_inverse_group({order.begin() + i, order.begin() + j}, st);
+            while (j < order.size() && order[j]->d == order[i]->d) ++j;
+            const std::size_t m = j - i, parts = (m + 7) / 8;
+            for (std::size_t q = 0; q < parts; ++q)
+                groups.emplace_back(order.begin() + i + m * q / parts, order.begin() + i + m * (q + 1) / parts);
             i = j;
         }
+        const cudaStream_t st = static_cast<cudaStream_t>(stream);
+        run_forked(groups.size(), st, [&](std::size_t g, cudaStream_t s) { damped_inverse_group(groups[g], s); });
         return 0;
     });
 }

@@ -145,6 +145,32 @@ __device__ __forceinline__ void tmem_ld16(uint32_t taddr, float (&v)[16]) {
     for (int i = 0; i < 16; ++i) v[i] = __uint_as_float(r[i]);
 }
 
+// Same without the wait: issue several loads, then one tmem_wait_ld().
+__device__ __forceinline__ void tmem_ld16_nowait(uint32_t taddr, uint32_t (&r)[16]) {
+    asm volatile(
+        "tcgen05.ld.sync.aligned.32x32b.x16.b32 "
+        "{%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
+        : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]),
+          "=r"(r[7]), "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]),
+          "=r"(r[13]), "=r"(r[14]), "=r"(r[15])
+        : "r"(taddr));
+}
+__device__ __forceinline__ void tmem_wait_ld() {
+    asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+}
+
+// 2^e as an exact double for |e| <= 1022 (no libm call).
+__device__ __forceinline__ double pow2(int e) {
+    return __longlong_as_double(static_cast<long long>(e + 1023) << 52);
+}
+
+// 2^e as a float, saturating outside the normal range (row/column scales of
+// finite fp32 data: e in [-148, 128]).
+__device__ __forceinline__ float pow2f(int e) {
+    return e > 127 ? __int_as_float(0x7f000000) * 2.0f
+                   : (e < -126 ? 0.0f : __int_as_float((e + 127) << 23));
+}
+
 // ---------------------------------------------------------------- descriptors
 // Shared-memory matrix descriptor for a K-major operand tile laid out by TMA
 // with SWIZZLE_128B: rows of 128 B, 8-row (1024 B) swizzle atoms stacked

@@ -50,7 +50,26 @@ __device__ __forceinline__ void valid_range(const SliceJob& J, int r, int& lo, i
     if (J.mode == SLICE_UPPER_BLOCK) lo = (r / 128) * 128;
 }
 
-// one warp per row; grid (ceil(rows / 8), jobs)
+__device__ __forceinline__ void slice_digits(float x, int e, int8_t (&q)[4], double& rep) {
+    float t = ldexpf(x, 7 - e);  // x * 2^-e * 2^7, |t| < 128 (exact: power-of-two scaling)
+    const float q0 = truncf(t);
+    t = (t - q0) * 128.0f;
+    const float q1 = truncf(t);
+    t = (t - q1) * 128.0f;
+    const float q2 = truncf(t);
+    t = (t - q2) * 128.0f;
+    const float q3 = fminf(fmaxf(rintf(t), -127.0f), 127.0f);
+    q[0] = static_cast<int8_t>(q0);
+    q[1] = static_cast<int8_t>(q1);
+    q[2] = static_cast<int8_t>(q2);
+    q[3] = static_cast<int8_t>(q3);
+    rep = static_cast<double>(q0) * 0x1p-7 + static_cast<double>(q1) * 0x1p-14 +
+          static_cast<double>(q2) * 0x1p-21 + static_cast<double>(q3) * 0x1p-28;
+}
+
+// one warp per row; grid (ceil(rows / 8), jobs).  Rows whose valid range is
+// 16-byte aligned move 4 elements per lane per access (float4 in, char4 out)
+// with 4 accesses in flight per lane.
 __global__ void __launch_bounds__(256) slice_kernel(const __grid_constant__ SliceBatch b) {
     const SliceJob& J = b.j[blockIdx.y];
     const int r = blockIdx.x * 8 + (threadIdx.x >> 5);
@@ -59,8 +78,29 @@ __global__ void __launch_bounds__(256) slice_kernel(const __grid_constant__ Slic
     int lo, hi;
     valid_range(J, r, lo, hi);
     const float* row = J.src + static_cast<int64_t>(r) * J.ld;
+    int8_t* p0 = J.planes + static_cast<int64_t>(r) * J.kpad;
+    const bool vec = ((reinterpret_cast<uintptr_t>(row + lo) & 15) == 0) && ((hi - lo) % 4 == 0) &&
+                     ((reinterpret_cast<uintptr_t>(p0 + lo) & 3) == 0) && (J.plane_stride % 4 == 0);
     float m = 0.0f;
-    for (int c = lo + lane; c < hi; c += 32) m = fmaxf(m, fabsf(row[c]));
+    if (vec) {
+        const float4* r4 = reinterpret_cast<const float4*>(row + lo);
+        const int n4 = (hi - lo) / 4;
+        int c = lane;
+        for (; c + 96 < n4; c += 128) {
+            float4 v[4];
+#pragma unroll
+            for (int u = 0; u < 4; ++u) v[u] = r4[c + 32 * u];
+#pragma unroll
+            for (int u = 0; u < 4; ++u)
+                m = fmaxf(m, fmaxf(fmaxf(fabsf(v[u].x), fabsf(v[u].y)), fmaxf(fabsf(v[u].z), fabsf(v[u].w))));
+        }
+        for (; c < n4; c += 32) {
+            const float4 v = r4[c];
+            m = fmaxf(m, fmaxf(fmaxf(fabsf(v.x), fabsf(v.y)), fmaxf(fabsf(v.z), fabsf(v.w))));
+        }
+    } else {
+        for (int c = lo + lane; c < hi; c += 32) m = fmaxf(m, fabsf(row[c]));
+    }
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, o));
     int e = 0;
@@ -70,24 +110,37 @@ __global__ void __launch_bounds__(256) slice_kernel(const __grid_constant__ Slic
         e = ex;          // so max|row| < 2^e
     }
     if (lane == 0) J.exps[r] = e;
-    int8_t* p0 = J.planes + static_cast<int64_t>(r) * J.kpad;
     double sq = 0.0;
-    for (int c = lo + lane; c < hi; c += 32) {
-        float t = ldexpf(row[c], 7 - e);  // x * 2^-e * 2^7, |t| < 128
-        const float q0 = truncf(t);
-        t = (t - q0) * 128.0f;
-        const float q1 = truncf(t);
-        t = (t - q1) * 128.0f;
-        const float q2 = truncf(t);
-        t = (t - q2) * 128.0f;
-        const float q3 = fminf(fmaxf(rintf(t), -127.0f), 127.0f);
-        p0[c] = static_cast<int8_t>(q0);
-        p0[c + J.plane_stride] = static_cast<int8_t>(q1);
-        p0[c + 2 * J.plane_stride] = static_cast<int8_t>(q2);
-        p0[c + 3 * J.plane_stride] = static_cast<int8_t>(q3);
-        const double rep = ldexp(static_cast<double>(q0), -7) + ldexp(static_cast<double>(q1), -14) +
-                           ldexp(static_cast<double>(q2), -21) + ldexp(static_cast<double>(q3), -28);
-        sq = fma(rep, rep, sq);
+    if (vec) {
+        const float4* r4 = reinterpret_cast<const float4*>(row + lo);
+        const int n4 = (hi - lo) / 4;
+        for (int c = lane; c < n4; c += 32) {
+            const float4 v = r4[c];
+            const float xs[4] = {v.x, v.y, v.z, v.w};
+            uint32_t packed[4] = {0u, 0u, 0u, 0u};
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+                int8_t q[4];
+                double rep;
+                slice_digits(xs[u], e, q, rep);
+                sq = fma(rep, rep, sq);
+#pragma unroll
+                for (int pl = 0; pl < 4; ++pl)
+                    packed[pl] |= static_cast<uint32_t>(static_cast<uint8_t>(q[pl])) << (8 * u);
+            }
+#pragma unroll
+            for (int pl = 0; pl < 4; ++pl)
+                *reinterpret_cast<uint32_t*>(p0 + lo + 4 * c + pl * J.plane_stride) = packed[pl];
+        }
+    } else {
+        for (int c = lo + lane; c < hi; c += 32) {
+            int8_t q[4];
+            double rep;
+            slice_digits(row[c], e, q, rep);
+            sq = fma(rep, rep, sq);
+#pragma unroll
+            for (int pl = 0; pl < 4; ++pl) p0[c + pl * J.plane_stride] = q[pl];
+        }
     }
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) sq += __shfl_xor_sync(0xffffffffu, sq, o);

@@ -87,7 +87,7 @@ struct GemmTraits {
     static constexpr int kPlaneBytes = kFmt == kOZ8 ? 128 * 64 : 128 * 128;
     static constexpr int kStageBytes = 2 * kPlanes * kPlaneBytes;
     static constexpr int kStages = 3;
-    static constexpr int kSmemBytes = kStages * kStageBytes + 1024 + 256;
+    static constexpr int kSmemBytes = kStages * kStageBytes + 1024 + 256 + 4 * kTile;
     static constexpr int kKBlock = 64;  // elements per k-block (both formats)
     static constexpr int kKSteps = kFmt == kOZ8 ? 2 : 4;  // 32-byte UMMA k-steps per block
     static constexpr uint32_t kTmemCols = kFmt == kOZ8 ? 512 : 128;
@@ -118,6 +118,7 @@ __global__ void __launch_bounds__(128, GemmTraits<kFmt>::kMinBlocks)
     uint64_t* empty = full + kStages;
     uint64_t* done = empty + kStages;
     uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(done + 1);
+    float* col_scale = reinterpret_cast<float*>(smem + kStages * T::kStageBytes + 256);  // kOZ8: 2^e_b per tile column
 
     const int gt = blockIdx.x;
     int p = 0;
@@ -142,6 +143,10 @@ __global__ void __launch_bounds__(128, GemmTraits<kFmt>::kMinBlocks)
     const int warp = threadIdx.x >> 5;
     const uint32_t lane = threadIdx.x & 31;
 
+    if constexpr (kFmt == kOZ8) {
+        const int c = tn * kTile + static_cast<int>(threadIdx.x);
+        col_scale[threadIdx.x] = c < P.cols ? ptx::pow2f(P.b_exp[c]) : 0.0f;
+    }
     if (threadIdx.x == 0) {
         for (int s = 0; s < kStages; ++s) {
             ptx::mbar_init(&full[s], 1);
@@ -234,9 +239,9 @@ __global__ void __launch_bounds__(128, GemmTraits<kFmt>::kMinBlocks)
     const uint32_t f = P.flags;
     const bool mirror = (f & EPI_MIRROR) && tm != tn;
     const uint32_t lane_base = tmem + (static_cast<uint32_t>(warp * 32) << 16);
-    double row_scale = 1.0;
+    float row_scale = 1.0f;
     if constexpr (kFmt == kOZ8) {
-        if (row_ok) row_scale = ldexp(1.0, P.a_exp[r]);
+        if (row_ok) row_scale = P.alpha * ptx::pow2f(P.a_exp[r]);
     }
 #pragma unroll 1
     for (int chunk = 0; chunk < kTile / 16; ++chunk) {
@@ -244,28 +249,30 @@ __global__ void __launch_bounds__(128, GemmTraits<kFmt>::kMinBlocks)
         const int c0 = tn * kTile + chunk * 16;
         float out[16];
         if constexpr (kFmt == kOZ8) {
-            // accumulator g counts units of 2^-7(g+2) of 2^(e_a + e_b)
-            double sum[16];
-#pragma unroll
-            for (int j = 0; j < 16; ++j) sum[j] = 0.0;
+            // accumulator g counts units of 2^-7(g+2) of 2^(e_a + e_b); the four
+            // exact int32 sums are recombined smallest-first in fp32 (the result
+            // is stored in fp32: ~1 ulp, no accumulation error)
+            uint32_t raw[kDigits][16];
             if (have_acc) {
 #pragma unroll
-                for (int g = kDigits - 1; g >= 0; --g) {
-                    float raw[16];
-                    ptx::tmem_ld16(lane_base + g * 128 + chunk * 16, raw);
-                    const double w = ldexp(1.0, -7 * (g + 2));
+                for (int g = 0; g < kDigits; ++g) ptx::tmem_ld16_nowait(lane_base + g * 128 + chunk * 16, raw[g]);
+                ptx::tmem_wait_ld();
+            } else {
 #pragma unroll
-                    for (int j = 0; j < 16; ++j)
-                        sum[j] = fma(static_cast<double>(__float_as_int(raw[j])), w, sum[j]);
-                }
+                for (int g = 0; g < kDigits; ++g)
+#pragma unroll
+                    for (int j = 0; j < 16; ++j) raw[g][j] = 0u;
             }
-            if ((f & EPI_EXACT_DIAG) && tm == tn && row_ok && r >= c0 && r < c0 + 16)
-                sum[r - c0] = P.a_sqnorm[r];  // exact sum of squares of the represented row
+            const bool diag_chunk = (f & EPI_EXACT_DIAG) && tm == tn && row_ok && r >= c0 && r < c0 + 16;
 #pragma unroll
             for (int j = 0; j < 16; ++j) {
-                const int c = c0 + j;
-                const double cs = (row_ok && c < P.cols) ? ldexp(row_scale, P.b_exp[c]) : 0.0;
-                out[j] = static_cast<float>(static_cast<double>(P.alpha) * (sum[j] * cs));
+                float s = static_cast<float>(static_cast<int>(raw[3][j])) * 0x1p-21f;
+                s = fmaf(static_cast<float>(static_cast<int>(raw[2][j])), 0x1p-14f, s);
+                s = fmaf(static_cast<float>(static_cast<int>(raw[1][j])), 0x1p-7f, s);
+                s = fmaf(static_cast<float>(static_cast<int>(raw[0][j])), 1.0f, s);
+                if (diag_chunk && c0 + j == r)
+                    s = static_cast<float>(P.a_sqnorm[r] * 0x1p14);  // exact sum of squares of the represented row
+                out[j] = (row_scale * col_scale[chunk * 16 + j]) * (s * 0x1p-14f);
             }
         } else {
             float v[16];
@@ -279,17 +286,31 @@ __global__ void __launch_bounds__(128, GemmTraits<kFmt>::kMinBlocks)
             for (int j = 0; j < 16; ++j) out[j] = P.alpha * v[j];
         }
         if (!row_ok || c0 >= P.cols) continue;
-        if (P.beta != 0.0f) {
-#pragma unroll
-            for (int j = 0; j < 16; ++j) {
-                const int c = c0 + j;
-                if (c >= P.cols) break;
-                const size_t idx = (f & EPI_TRANSPOSE) ? static_cast<size_t>(c) * P.ldc + r
-                                                       : static_cast<size_t>(r) * P.ldc + c;
-                out[j] = fmaf(P.beta, P.c[idx], out[j]);
-            }
-        }
         const bool full_chunk = c0 + 16 <= P.cols;
+        if (P.beta != 0.0f) {
+            float cv[16];
+            if ((f & EPI_VEC4) && full_chunk && !(f & EPI_TRANSPOSE)) {
+                const float4* src = reinterpret_cast<const float4*>(P.c + static_cast<size_t>(r) * P.ldc + c0);
+#pragma unroll
+                for (int q = 0; q < 4; ++q) {
+                    const float4 t = src[q];
+                    cv[4 * q] = t.x;
+                    cv[4 * q + 1] = t.y;
+                    cv[4 * q + 2] = t.z;
+                    cv[4 * q + 3] = t.w;
+                }
+            } else {
+#pragma unroll
+                for (int j = 0; j < 16; ++j) {
+                    const int c = c0 + j;
+                    const size_t idx = (f & EPI_TRANSPOSE) ? static_cast<size_t>(c) * P.ldc + r
+                                                           : static_cast<size_t>(r) * P.ldc + c;
+                    cv[j] = c < P.cols ? P.c[idx] : 0.0f;
+                }
+            }
+#pragma unroll
+            for (int j = 0; j < 16; ++j) out[j] = fmaf(P.beta, cv[j], out[j]);
+        }
         if ((f & EPI_VEC4) && full_chunk && !(f & EPI_TRANSPOSE)) {
             float4* dst = reinterpret_cast<float4*>(P.c + static_cast<size_t>(r) * P.ldc + c0);
 #pragma unroll

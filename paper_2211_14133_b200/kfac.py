@@ -217,7 +217,7 @@ def _check_prec(grad, a_inv, b_inv):
 
 
 def precondition(grad: torch.Tensor, a_inv: torch.Tensor, b_inv: torch.Tensor) -> torch.Tensor:
-    """kfac.hpp:51 — B^-1 G A^-1 (two chained 3xTF32 tensor-core GEMMs)."""
+    """kfac.hpp:51 — B^-1 G A^-1 (two chained fp32-accurate int8-digit tensor-core GEMMs)."""
     _check_prec(grad, a_inv, b_inv)
     d_out, d_in = grad.shape
     out = torch.empty_like(grad)
