@@ -2,7 +2,7 @@
  *
  * Each entry point replaces one reference function of
  * /root/reference/proj/include/pipefill/kfac/{kfac,matrix}.hpp; the C++
- * wrapper layer (include/pipefill/kfac/*.hpp, csrc/host/kfac_host.cpp) and the
+ * wrapper layer (include/pipefill/kfac/{matrix,kfac}.hpp, csrc/host/kfac_host.cpp) and the
  * Python mirror (paper_2211_14133_b200/kfac.py) restore the reference's
  * value-semantics signatures on top of these.
  *

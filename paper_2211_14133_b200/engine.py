@@ -1,0 +1,353 @@
+"""PipeFisher trainer: BERT stages + K-FAC state + the runtime (runtime.py).
+
+``CudaBackend`` is the product backend: F/B of the hosted BERT stages on the
+compute stream (torch / cuBLAS — the bubble-creating work), every K-FAC
+operation through libpf_b200.so (kfac.py): grouped tcgen05 SYRK curvature,
+batched fp32-accurate damped inverses written in digit form, and the grouped
+fused precondition-update.  Nothing here has a CPU path.
+
+Per hosted stage and encoder layer the factor sets are:
+  A-set: a_qkv (Q/K/V share one input), a_o, a_ffn1, a_ffn2   -> 4 factors
+  B-set: e_q, e_k, e_v, e_o, e_ffn1, e_ffn2                    -> 6 factors
+"""
+from __future__ import annotations
+
+import time
+from dataclasses import dataclass
+from typing import Dict, List, Optional, Tuple
+
+import torch
+
+from . import kfac as K
+from . import runtime as R
+from . import schedule as S
+from .bert import BertConfig, BertStage, synthetic_batch
+
+A_KEYS = ("a_qkv", "a_o", "a_ffn1", "a_ffn2")
+E_KEYS = ("e_q", "e_k", "e_v", "e_o", "e_ffn1", "e_ffn2")
+LINEAR_FACTORS = {"q": ("a_qkv", "e_q"), "k": ("a_qkv", "e_k"), "v": ("a_qkv", "e_v"),
+                  "o": ("a_o", "e_o"), "ffn1": ("a_ffn1", "e_ffn1"), "ffn2": ("a_ffn2", "e_ffn2")}
+
+
+def factor_dim(bert: BertConfig, key: str) -> int:
+    return bert.ffn if key in ("a_ffn2", "e_ffn1") else bert.hidden
+
+
+class StageKfac:
+    """Factors, double-buffered inverses (fp32 + digit form) and the
+    per-cycle accumulation state of one hosted stage."""
+
+    def __init__(self, bert: BertConfig, layers: int, device):
+        self.bert, self.layers = bert, layers
+        self.factor: Dict[Tuple[int, str], torch.Tensor] = {}
+        self.inv: Dict[Tuple[int, str, int], K.SlicedMatrix] = {}
+        for l in range(layers):
+            for key in A_KEYS + E_KEYS:
+                d = factor_dim(bert, key)
+                self.factor[(l, key)] = torch.zeros((d, d), dtype=torch.float32, device=device)
+                for slot in (0, 1):
+                    self.inv[(l, key, slot)] = K.SlicedMatrix(
+                        torch.zeros((d, d), dtype=torch.float32, device=device),
+                        torch.zeros(K.slice_bytes(d, d), dtype=torch.uint8, device=device))
+        self.version = {(l, f): -1 for l in range(layers) for f in (0, 1)}  # -1: no inverse yet
+        self.started = {(l, f): False for l in range(layers) for f in (0, 1)}
+        self.slot_free: Dict[Tuple[int, int, int], Optional[torch.cuda.Event]] = {}
+        self.inv_ready: Optional[torch.cuda.Event] = None
+
+    @staticmethod
+    def keys(f: int):
+        return A_KEYS if f == 0 else E_KEYS
+
+
+class CudaBackend:
+    def __init__(self, topo: R.Topology, bert: BertConfig, rank: int, device, kfac: bool = True,
+                 damping: float = 0.1, lr: float = 1e-3, seed: int = 0):
+        cfg = topo.cfg
+        self.topo, self.bert, self.rank, self.device, self.use_kfac = topo, bert, rank, device, kfac
+        self.damping, self.lr = damping, lr
+        self.B, self.Sq, L = cfg.micro_batch_size, cfg.seq_len, cfg.layers_per_stage
+        self.tokens = self.B * self.Sq
+        self.compute = torch.cuda.current_stream(device)
+        self.kfac_stream = torch.cuda.Stream(device=device, priority=0)  # low priority (torch: 0 = lowest)
+        torch.manual_seed(seed + 1000 * rank)
+        self.stages: Dict[int, BertStage] = {}
+        self.kstate: Dict[int, StageKfac] = {}
+        for s in topo.stages_on(rank):
+            torch.manual_seed(seed + s)  # replicas of a stage start identical
+            st = BertStage(bert, s * L, L, s == 0, s == topo.D - 1).to(device)
+            self.stages[s] = st
+            if kfac:
+                self.kstate[s] = StageKfac(bert, L, device)
+        # micro-batches this device runs (its pipe's half under Chimera)
+        self.local_micros = {s: sum(1 for m in range(cfg.micro_batches)
+                                    if topo.device(topo.pipe_of(m), s, rank // topo.D) == rank)
+                             for s in self.stages}
+        self.data = {m: synthetic_batch(bert, self.B, self.Sq, seed + 7919 * (rank // topo.D) + m, device)
+                     for m in range(cfg.micro_batches)}
+        self.saved: Dict[Tuple[int, int], Tuple] = {}
+        self.losses: List[torch.Tensor] = []
+        self.timeline: List[Tuple[str, torch.cuda.Event, torch.cuda.Event]] = []
+        self.record = False
+
+    # ------------------------------------------------------------ timing helpers
+    def _begin(self, stream):
+        if not self.record:
+            return None
+        e = torch.cuda.Event(enable_timing=True)
+        e.record(stream)
+        return e
+
+    def _end(self, kind, e0, stream):
+        if e0 is None:
+            return
+        e1 = torch.cuda.Event(enable_timing=True)
+        e1.record(stream)
+        self.timeline.append((kind, e0, e1))
+
+    def mark_compute(self):
+        ev = torch.cuda.Event()
+        ev.record(self.compute)
+        return ev
+
+    def act_shape(self, stage, micro):
+        return (self.B, self.Sq, self.bert.hidden), torch.bfloat16
+
+    # ------------------------------------------------------------ F / B
+    def forward(self, stage, micro, x, capture, cycle):
+        mod = self.stages[stage]
+        e0 = self._begin(self.compute)
+        ids, pos, labels = self.data[micro]
+        if mod.is_first:
+            inp = ids
+        else:
+            inp = x.requires_grad_()
+        mod.store.active_micro = micro if (capture and self.use_kfac) else None
+        out = mod(inp, pos, labels)
+        mod.store.active_micro = None
+        self.saved[(stage, micro)] = (inp, out)
+        self._end("F", e0, self.compute)
+        if mod.is_last:
+            self.losses.append(out.detach())
+            return None
+        return out.detach().to(torch.bfloat16)
+
+    def backward(self, stage, micro, gy, capture):
+        mod = self.stages[stage]
+        e0 = self._begin(self.compute)
+        inp, out = self.saved.pop((stage, micro))
+        mod.store.active_micro = micro if (capture and self.use_kfac) else None
+        if mod.is_last:
+            (out / self.local_micros[stage]).backward()
+        else:
+            out.backward(gy.to(out.dtype))
+        mod.store.active_micro = None
+        self._end("B", e0, self.compute)
+        return None if mod.is_first else inp.grad.to(torch.bfloat16)
+
+    # ------------------------------------------------------------ K-FAC items
+    def curvature(self, stage, layer, f, micro, gate):
+        ks, mod = self.kstate[stage], self.stages[stage]
+        with torch.cuda.stream(self.kfac_stream):
+            if gate is not None:
+                self.kfac_stream.wait_event(gate)
+            e0 = self._begin(self.kfac_stream)
+            scale = 1.0 / (self.local_micros[stage] * self.tokens)
+            probs = []
+            for key in ks.keys(f):
+                x = mod.store.get(layer, key, micro)
+                x.record_stream(self.kfac_stream)
+                probs.append((x, ks.factor[(layer, key)], scale, ks.started[(layer, f)]))
+            K.syrk(probs, fill_upper=False)  # one grouped tcgen05 launch per work item
+            ks.started[(layer, f)] = True
+            self._end("CURV", e0, self.kfac_stream)
+
+    def sync_curvature(self, stage, layer, f, group, gate):
+        ks = self.kstate[stage]
+        with torch.cuda.stream(self.kfac_stream):
+            if gate is not None:
+                self.kfac_stream.wait_event(gate)
+            e0 = self._begin(self.kfac_stream)
+            if group is not None:
+                import torch.distributed as dist
+                for key in ks.keys(f):
+                    dist.all_reduce(ks.factor[(layer, key)], op=dist.ReduceOp.AVG, group=group)
+            self._end("SYNC_CURV", e0, self.kfac_stream)
+
+    def invert(self, stage, layer, f, gate):
+        ks = self.kstate[stage]
+        slot = (ks.version[(layer, f)] + 1) % 2
+        with torch.cuda.stream(self.kfac_stream):
+            if gate is not None:
+                self.kfac_stream.wait_event(gate)
+            free = ks.slot_free.get((layer, f, slot))
+            if free is not None:  # last precondition that read this slot
+                self.kfac_stream.wait_event(free)
+            e0 = self._begin(self.kfac_stream)
+            keys = ks.keys(f)
+            mats = [ks.factor[(layer, k)] for k in keys]
+            outs = [ks.inv[(layer, k, slot)] for k in keys]
+            K.damped_inverse_batched(mats, self.damping, [o.fp32 for o in outs], [o.digits for o in outs],
+                                     check=False)
+            self._end("INV", e0, self.kfac_stream)
+            ev = torch.cuda.Event()
+            ev.record(self.kfac_stream)
+        ks.version[(layer, f)] += 1
+        ks.started[(layer, f)] = False
+        ks.inv_ready = ev
+
+    def broadcast_inverse(self, stage, layer, f, owner, group, gate):
+        ks = self.kstate[stage]
+        import torch.distributed as dist
+        if owner != self.rank:
+            ks.version[(layer, f)] += 1
+        slot = ks.version[(layer, f)] % 2
+        with torch.cuda.stream(self.kfac_stream):
+            if gate is not None:
+                self.kfac_stream.wait_event(gate)
+            for key in ks.keys(f):
+                m = ks.inv[(layer, key, slot)]
+                dist.broadcast(m.fp32, src=owner, group=group)
+                dist.broadcast(m.digits, src=owner, group=group)
+            ev = torch.cuda.Event()
+            ev.record(self.kfac_stream)
+        ks.inv_ready = ev
+
+    def sync_grad(self, stage, group):
+        if group is None:
+            return
+        import torch.distributed as dist
+        e0 = self._begin(self.compute)
+        grads = [p.grad for p in self.stages[stage].parameters() if p.grad is not None]
+        flat = torch.cat([g.reshape(-1) for g in grads])
+        dist.all_reduce(flat, op=dist.ReduceOp.AVG, group=group)
+        off = 0
+        for g in grads:
+            g.copy_(flat[off:off + g.numel()].view_as(g))
+            off += g.numel()
+        self._end("SYNC_GRAD", e0, self.compute)
+
+    def precondition(self, stage, step):
+        mod = self.stages[stage]
+        e0 = self._begin(self.compute)
+        kfac_params = set()
+        if self.use_kfac:
+            ks = self.kstate[stage]
+            if ks.inv_ready is not None:
+                self.compute.wait_event(ks.inv_ready)
+                ks.inv_ready = None
+            items = []
+            for l, layer in enumerate(mod.kfac_layers()):
+                va, vb = ks.version[(l, 0)], ks.version[(l, 1)]
+                for name, (ak, ek) in LINEAR_FACTORS.items():
+                    w = layer.w[name]
+                    kfac_params.add(id(w))
+                    if w.grad is None:
+                        continue
+                    if va < 0 or vb < 0:  # no inverse yet: the plain gradient (A.13)
+                        w.data.add_(w.grad, alpha=-self.lr)
+                        continue
+                    items.append((w.data, w.grad, ks.inv[(l, ak, va % 2)], ks.inv[(l, ek, vb % 2)], self.lr))
+            K.precondition_update_sliced(items)  # W -= eta B^-1 G A^-1, one grouped call
+            done = torch.cuda.Event()
+            done.record(self.compute)
+            for l in range(ks.layers):
+                for f in (0, 1):
+                    v = ks.version[(l, f)]
+                    if v >= 0:
+                        ks.slot_free[(l, f, v % 2)] = done
+        with torch.no_grad():
+            for p in mod.parameters():
+                if p.grad is not None and id(p) not in kfac_params:
+                    p.add_(p.grad, alpha=-self.lr)
+                p.grad = None
+        self._end("PREC", e0, self.compute)
+
+    def end_cycle(self):
+        for mod in self.stages.values():
+            mod.store.clear()
+
+
+@dataclass
+class CycleResult:
+    cycle_ms: float
+    step_ms: float
+    util: float
+    busy_ms: float
+    loss: Optional[float]
+
+
+class PipeFisherTrainer:
+    """Topology + schedule + program + backend for THIS rank."""
+
+    def __init__(self, cfg: S.PipelineConfig, bert: BertConfig, rank: int = 0, world: int = 1,
+                 device=None, kfac: bool = True, refresh: int = 2, costs: Optional[S.CostTable] = None,
+                 damping: float = 0.1, lr: float = 1e-3, seed: int = 0, dist=None,
+                 inversion_parallel: bool = False):
+        self.cfg, self.bert, self.rank, self.world = cfg, bert, rank, world
+        self.topo = R.Topology(cfg)
+        if self.topo.n_devices() != world:
+            raise ValueError(f"config needs {self.topo.n_devices()} devices, world is {world}")
+        self.device = device or torch.device("cuda", torch.cuda.current_device())
+        self.backend = CudaBackend(self.topo, bert, rank, self.device, kfac, damping, lr, seed)
+        self.filled = None
+        if cfg.stages == 1 and cfg.replicas == 1:
+            prog = R.inline_program(cfg, refresh)
+            progs = [prog]
+        else:
+            costs = costs or S.CostTable(t_f=1.0, t_b=2.0, t_curv=0.05, t_inv=0.3, t_prec=0.1)
+            base = S.build_schedule(cfg, costs)
+            self.filled = S.assign_works(base, cfg, costs, S.enumerate_kfac_works(cfg, costs),
+                                         S.AssignOptions(inversion_parallel=inversion_parallel))
+            progs = R.device_programs(self.filled, cfg, inversion_broadcast=inversion_parallel)
+        if not kfac:
+            progs = [[o for o in p if o.kind in (R.F_, R.B_, R.SYNC_GRAD, R.PREC)] for p in progs]
+            for p in progs:
+                R._assign_gates(p)
+        self.programs = progs
+        self.program = progs[rank]
+        self.refresh = max((o.step for o in self.program), default=0) + 1
+        self.comm = None
+        if world > 1:
+            replica_sets = [self.topo.replicas(s) for s in range(cfg.stages)]
+            self.comm = R.Comm(dist, rank, R.channel_plan(progs), replica_sets, self.device)
+        self.executor = R.Executor(self.program, self.backend, self.comm or _LocalComm(), rank)
+        self.cycles = 0
+
+    def run_cycle(self, record: bool = False) -> CycleResult:
+        b = self.backend
+        b.record = record
+        b.timeline.clear()
+        b.losses.clear()
+        t0 = torch.cuda.Event(enable_timing=True)
+        t1 = torch.cuda.Event(enable_timing=True)
+        t0.record(b.compute)
+        self.executor.run_cycle(self.cycles)
+        if self.comm:
+            self.comm.flush()
+        b.compute.wait_stream(b.kfac_stream)
+        t1.record(b.compute)
+        torch.cuda.synchronize(self.device)
+        self.cycles += 1
+        cycle_ms = t0.elapsed_time(t1)
+        busy = 0.0
+        if record and b.timeline:
+            iv = sorted((t0.elapsed_time(e0), t0.elapsed_time(e1)) for _, e0, e1 in b.timeline)
+            cur_b, cur_e = iv[0]
+            for s, e in iv[1:]:
+                if s > cur_e:
+                    busy += cur_e - cur_b
+                    cur_b, cur_e = s, e
+                else:
+                    cur_e = max(cur_e, e)
+            busy += cur_e - cur_b
+        loss = float(torch.stack(b.losses).mean()) if b.losses else None
+        return CycleResult(cycle_ms, cycle_ms / self.refresh, busy / cycle_ms if cycle_ms > 0 else 0.0,
+                           busy, loss)
+
+
+class _LocalComm:
+    def group(self, devs):
+        return None
+
+    def flush(self):
+        pass

@@ -1,0 +1,215 @@
+"""Pipeline runtime (paper_2211_14133_b200/runtime.py): the per-device
+programs derived from the reference assigner's FilledSchedule, checked for
+conservation, communication consistency (deadlock freedom by construction)
+and K-FAC dependency order; then executed for real over torch.distributed
+(gloo, world size 2 and 4) with a recording test backend."""
+import os
+import socket
+from collections import Counter
+
+import pytest
+import torch
+import torch.distributed as dist
+import torch.multiprocessing as mp
+
+from paper_2211_14133_b200 import runtime as R
+from paper_2211_14133_b200 import schedule as S
+
+CASES = [
+    ("gpipe_d4n4", S.Method.GPipe, 4, 4, 1, 3),
+    ("1f1b_d4n4_w2", S.Method.OneF1B, 4, 4, 2, 6),
+    ("chimera_d4n4", S.Method.Chimera, 4, 4, 2, 3),
+    ("chimera_d8n8", S.Method.Chimera, 8, 8, 2, 3),
+    ("gpipe_d2n2_w2", S.Method.GPipe, 2, 2, 2, 1),
+]
+COSTS = S.CostTable(t_f=1.0, t_b=2.0, t_curv=0.05, t_inv=0.3, t_prec=0.1)
+
+
+def build(method, D, N, W, L, inv_par=False):
+    cfg = S.PipelineConfig(method=method, stages=D, micro_batches=N, micro_batch_size=32,
+                           replicas=W, layers_per_stage=L)
+    base = S.build_schedule(cfg, COSTS)
+    filled = S.assign_works(base, cfg, COSTS, S.enumerate_kfac_works(cfg, COSTS),
+                            S.AssignOptions(inversion_parallel=inv_par))
+    return cfg, filled, R.device_programs(filled, cfg, inversion_broadcast=inv_par)
+
+
+@pytest.mark.parametrize("name,method,D,N,W,L", CASES)
+def test_programs_conserve_the_filled_schedule(name, method, D, N, W, L):
+    cfg, filled, progs = build(method, D, N, W, L)
+    assert len(progs) == cfg.effective_devices()
+    for dev, (p, line) in enumerate(zip(progs, filled.schedule.timelines)):
+        got = Counter(o.key() for o in p if not o.synthetic)
+        want = Counter((R._KIND[w.kind], w.stage, w.micro_batch, w.layer,
+                        None if w.factor is None else int(w.factor), w.step) for w in line)
+        assert got == want, dev
+        starts = [o.start for o in p if not o.synthetic]
+        assert starts == sorted(starts)
+
+
+@pytest.mark.parametrize("name,method,D,N,W,L", CASES)
+def test_channels_fifo_and_collectives_ordered(name, method, D, N, W, L):
+    _, _, progs = build(method, D, N, W, L)
+    R.check_channel_fifo(progs)
+    R.check_collective_order(progs)
+
+
+@pytest.mark.parametrize("inv_par", [False, True])
+def test_chimera_inversion_parallel_broadcasts_consistent(inv_par):
+    _, _, progs = build(S.Method.Chimera, 4, 4, 2, 3, inv_par)
+    R.check_collective_order(progs)
+    n_b = sum(o.kind == "BCAST_INV" for p in progs for o in p)
+    n_inv = sum(o.kind == R.INV for p in progs for o in p)
+    assert n_b == (2 * n_inv if inv_par else 0)  # every replica joins each broadcast
+
+
+@pytest.mark.parametrize("name,method,D,N,W,L", CASES)
+def test_kfac_dependencies_respected(name, method, D, N, W, L):
+    """Curvature after its anchor F/B (gate), Sync/Inversion after the
+    device's curvature of that (stage, layer, factor), Precondition after
+    SyncGrad of its stage and the stage's last backward."""
+    _, _, progs = build(method, D, N, W, L)
+    for p in progs:
+        seen_curv = Counter()
+        for i, o in enumerate(p):
+            if o.kind in R.KFAC_STREAM_OPS:
+                assert o.gate is not None and o.gate < i and p[o.gate].kind in (R.F_, R.B_)
+            if o.kind == R.CURV:
+                seen_curv[(o.stage, o.layer, o.factor)] += 1
+                if o.step == 0:
+                    # the anchor F (A-set) / B (B-set) of this micro already ran in step 0
+                    anchor = R.F_ if o.factor == 0 else R.B_
+                    assert any(q.kind == anchor and q.micro == o.micro and q.stage == o.stage and q.step == 0
+                               for q in p[:i])
+            if o.kind in (R.SYNC_CURV, R.INV):
+                later = [q for q in p[i + 1:] if q.kind == R.CURV and q.step == o.step and
+                         (q.stage, q.layer, q.factor) == (o.stage, o.layer, o.factor)]
+                assert not later
+            if o.kind == R.PREC:
+                fbs = [q for q in p[:i] if q.kind == R.B_ and q.stage == o.stage and q.step == o.step]
+                assert fbs, "precondition before the stage's backward"
+
+
+def test_inline_program_single_device():
+    cfg = S.PipelineConfig(stages=1, micro_batches=4, layers_per_stage=24)
+    prog = R.inline_program(cfg, refresh=2)
+    kinds = Counter(o.kind for o in prog)
+    assert kinds[R.F_] == kinds[R.B_] == 8
+    assert kinds[R.CURV] == 4 * 24 * 2 and kinds[R.INV] == 24 * 2 and kinds[R.PREC] == 2
+    # 1F1B on one device: F0 B0 F1 B1 ...
+    fb = [(o.kind, o.micro) for o in prog if o.kind in (R.F_, R.B_) and o.step == 0]
+    assert fb == [(R.F_, 0), (R.B_, 0), (R.F_, 1), (R.B_, 1), (R.F_, 2), (R.B_, 2), (R.F_, 3), (R.B_, 3)]
+    with pytest.raises(ValueError):
+        R.inline_program(S.PipelineConfig(stages=2, micro_batches=2), 1)
+
+
+# ---------------------------------------------------------------- real execution (gloo)
+class RecordingBackend:
+    """Test double: F/B move tagged tensors so the receiver can verify it got
+    the right micro-batch of the right stage; K-FAC ops are recorded."""
+
+    def __init__(self, rank, topo):
+        self.rank, self.topo = rank, topo
+        self.log = []
+
+    def act_shape(self, stage, micro):
+        return (4,), torch.float32
+
+    def mark_compute(self):
+        return ("done", len(self.log))
+
+    def forward(self, stage, micro, x, capture, cycle):
+        if stage > 0:
+            assert x.tolist() == [stage - 1, micro, 0, cycle], (stage, micro, x)
+        self.log.append(("F", stage, micro))
+        return torch.tensor([stage, micro, 0, cycle], dtype=torch.float32)
+
+    def backward(self, stage, micro, gy, capture):
+        if stage < self.topo.D - 1:
+            assert gy.tolist() == [stage + 1, micro, 1, 0], (stage, micro, gy)
+        self.log.append(("B", stage, micro))
+        return torch.tensor([stage, micro, 1, 0], dtype=torch.float32)
+
+    def curvature(self, stage, layer, f, micro, gate):
+        assert gate is not None
+        self.log.append(("CURV", stage, layer, f, micro))
+
+    def sync_curvature(self, stage, layer, f, group, gate):
+        t = torch.tensor([float(self.rank)])
+        dist.all_reduce(t, group=group)
+        self.log.append(("SYNC_CURV", stage, layer, f, t.item()))
+
+    def invert(self, stage, layer, f, gate):
+        self.log.append(("INV", stage, layer, f))
+
+    def broadcast_inverse(self, stage, layer, f, owner, group, gate):
+        t = torch.tensor([float(self.rank)])
+        dist.broadcast(t, src=owner, group=group)
+        assert t.item() == owner
+        self.log.append(("BCAST", stage, layer, f))
+
+    def sync_grad(self, stage, group):
+        t = torch.tensor([1.0])
+        dist.all_reduce(t, group=group)
+        self.log.append(("SYNC_GRAD", stage, t.item()))
+
+    def precondition(self, stage, step):
+        self.log.append(("PREC", stage, step))
+
+    def end_cycle(self):
+        pass
+
+
+def _worker(rank, world, port, method, D, N, W, L, inv_par, q):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        cfg, filled, progs = build(method, D, N, W, L, inv_par)
+        topo = R.Topology(cfg)
+        comm = R.Comm(dist, rank, R.channel_plan(progs), [topo.replicas(s) for s in range(D)])
+        be = RecordingBackend(rank, topo)
+        ex = R.Executor(progs[rank], be, comm, rank)
+        for cycle in range(2):
+            ex.run_cycle(cycle)
+            comm.flush()
+        q.put((rank, be.log))
+    finally:
+        dist.destroy_process_group()
+
+
+def _free_port():
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        return s.getsockname()[1]
+
+
+@pytest.mark.parametrize("method,D,N,W,L,inv_par", [
+    (S.Method.GPipe, 2, 2, 1, 1, False),
+    (S.Method.OneF1B, 2, 4, 1, 2, False),
+    (S.Method.Chimera, 4, 4, 2, 1, False),   # world 4: both pipes, SyncCurvature + SyncGrad
+    (S.Method.GPipe, 2, 2, 2, 1, True),      # world 4: data-parallel replicas, inverse broadcast
+])
+def test_gloo_execution_no_deadlock_and_data_routed(method, D, N, W, L, inv_par):
+    cfg = S.PipelineConfig(method=method, stages=D, micro_batches=N, replicas=W, layers_per_stage=L)
+    world = cfg.effective_devices()
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_worker, args=(r, world, port, method, D, N, W, L, inv_par, q))
+             for r in range(world)]
+    for p in procs:
+        p.start()
+    logs = {}
+    for _ in range(world):
+        r, log = q.get(timeout=120)
+        logs[r] = log
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    _, _, progs = build(method, D, N, W, L, inv_par)
+    for r in range(world):
+        n_ops = sum(1 for o in progs[r])
+        assert len(logs[r]) == 2 * n_ops
+        syncs = [e for e in logs[r] if e[0] == "SYNC_CURV"]
+        if W > 1 or method == S.Method.Chimera:
+            assert syncs and all(e[-1] > 0 for e in syncs)  # every replica joined
