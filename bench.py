@@ -342,6 +342,8 @@ def run_gpu_arm(args, rank, world, local_rank):
         e2e_ms = float(t.item())
     e2e_value = job_flops / (e2e_ms * 1e-3) / 1e12
 
+    pipeline = None if args.no_pipeline else pipeline_section(args, rank, world, local_rank, dist)
+
     if rank != 0:
         if dist: dist.destroy_process_group()
         return
@@ -391,9 +393,84 @@ def run_gpu_arm(args, rank, world, local_rank):
         "gpu_launches": launches // max(1, args.steps) if False else launches,
         "clocks": clocks.summary(),
         "cpu_baseline": cpu,
+        "pipeline": pipeline,
     }
     print(json.dumps(line), flush=True)
     if dist: dist.destroy_process_group()
+
+
+# ====================================================================== pipeline step
+PIPELINE_LADDER = {  # SURVEY §8d 1/2/4/8-GPU ladder (BERT-Large, micro-batch 32 x 128)
+    1: dict(method="gpipe", stages=1, micro_batches=4, replicas=1),      # inline K-FAC (no bubbles)
+    2: dict(method="gpipe", stages=2, micro_batches=4, replicas=1),
+    4: dict(method="gpipe", stages=4, micro_batches=4, replicas=1),
+    8: dict(method="chimera", stages=8, micro_batches=8, replicas=2),    # BASELINE configs[2]
+}
+
+
+def pipeline_costs(cfg, layers_per_stage):
+    """CostTable for the assigner from this build's measured kernel rates
+    (DESIGN.md §3): F = l x 105 GFLOP at ~600 TFLOP/s, B = 2F, one set's SYRK
+    per micro-batch ~0.1 ms, one set's inversion ~3.2 ms, precondition
+    ~0.6 ms per encoder layer."""
+    from paper_2211_14133_b200 import schedule as S
+    spd = 2 if cfg.method == S.Method.Chimera else 1
+    t_f = layers_per_stage * 0.175
+    return S.CostTable(t_f=t_f, t_b=2 * t_f, t_curv=0.1, t_inv=layers_per_stage * 3.2,
+                       t_prec=spd * layers_per_stage * 0.6)
+
+
+def pipeline_section(args, rank, world, local_rank, dist):
+    import torch
+    from paper_2211_14133_b200 import schedule as S
+    from paper_2211_14133_b200.bert import BertConfig
+    from paper_2211_14133_b200.engine import PipeFisherTrainer
+    spec = PIPELINE_LADDER.get(world)
+    if spec is None:
+        return {"skipped": f"no ladder entry for {world} GPUs"}
+    bert = BertConfig.large()
+    method = S.parse_method(spec["method"])
+    spd = 2 if method == S.Method.Chimera else 1
+    L = bert.layers // spec["stages"]
+    cfg = S.PipelineConfig(method=method, stages=spec["stages"], micro_batches=spec["micro_batches"],
+                           micro_batch_size=32, replicas=spec["replicas"], layers_per_stage=L, seq_len=128)
+    costs = pipeline_costs(cfg, L)
+    out = {"model": "BERT-Large (24 x 1024, FFN 4096, 16 heads), random init", "method": spec["method"],
+           "stages": cfg.stages, "micro_batches": cfg.micro_batches, "micro_batch": "32 x 128",
+           "replicas": cfg.replicas, "layers_per_stage": L, "data": "synthetic token ids, 15% MLM"}
+
+    def measure(kfac):
+        t = PipeFisherTrainer(cfg, bert, rank, world, torch.device("cuda", local_rank), kfac=kfac,
+                              refresh=2, costs=costs, dist=dist, seed=11)
+        t.run_cycle()  # warm-up (allocations, cuBLAS heuristics)
+        if dist: dist.barrier()
+        res = [t.run_cycle(record=(i == 1)) for i in range(2)]
+        step = statistics.mean(r.step_ms for r in res)
+        util = res[1].util
+        info = {"refresh_period": t.refresh}
+        if t.filled is not None:
+            m = S.schedule_metrics(t.filled.schedule)
+            info["simulated_util"] = m[1] if isinstance(m, tuple) else getattr(m, "utilization", None)
+        if dist:
+            x = torch.tensor([step, -util], device="cuda")
+            dist.all_reduce(x, op=dist.ReduceOp.MAX)
+            step, util = float(x[0]), -float(x[1])  # max step time, min util over ranks
+        loss = res[-1].loss
+        del t
+        torch.cuda.empty_cache()
+        return step, util, loss, info
+
+    try:
+        plain_ms, plain_util, _, _ = measure(False)
+        step_ms, util, loss, info = measure(True)
+        seqs = cfg.micro_batches * cfg.micro_batch_size * cfg.groups() * (2 if spd == 2 else 1) / spd
+        out.update({"step_ms": step_ms, "plain_step_ms": plain_ms, "step_ratio_vs_plain": step_ms / plain_ms,
+                    "gpu_util": util, "plain_gpu_util": plain_util,
+                    "sequences_per_s": seqs / (step_ms * 1e-3), "loss": loss, **info,
+                    "util_definition": "union of F/B/K-FAC/collective op intervals (CUDA events) / cycle wall time, min over ranks"})
+    except Exception as e:  # reported, never fatal for the bench line
+        out["error"] = f"{type(e).__name__}: {e}"[:400]
+    return out
 
 
 def main():
@@ -404,6 +481,7 @@ def main():
     p.add_argument("--impl", default="ours", choices=["ours", "reference"])
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--no-graph", action="store_true", help="eager launches instead of a CUDA graph")
+    p.add_argument("--no-pipeline", action="store_true", help="skip the BERT-Large pipeline step section")
     args = p.parse_args()
     rank = int(os.environ.get("RANK", "0"))
     world = int(os.environ.get("WORLD_SIZE", str(args.gpus)))

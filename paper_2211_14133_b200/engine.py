@@ -67,8 +67,13 @@ class CudaBackend:
         self.damping, self.lr = damping, lr
         self.B, self.Sq, L = cfg.micro_batch_size, cfg.seq_len, cfg.layers_per_stage
         self.tokens = self.B * self.Sq
-        self.compute = torch.cuda.current_stream(device)
-        self.kfac_stream = torch.cuda.Stream(device=device, priority=0)  # low priority (torch: 0 = lowest)
+        low, high = torch.cuda.Stream.priority_range()
+        # F/B (and the tail) on a high-priority stream made current for torch;
+        # K-FAC items on a low-priority stream: when both have CTAs pending the
+        # block scheduler serves F/B first
+        self.compute = torch.cuda.Stream(device=device, priority=high)
+        torch.cuda.set_stream(self.compute)
+        self.kfac_stream = torch.cuda.Stream(device=device, priority=low)
         torch.manual_seed(seed + 1000 * rank)
         self.stages: Dict[int, BertStage] = {}
         self.kstate: Dict[int, StageKfac] = {}
@@ -146,19 +151,33 @@ class CudaBackend:
 
     # ------------------------------------------------------------ K-FAC items
     def curvature(self, stage, layer, f, micro, gate):
-        ks, mod = self.kstate[stage], self.stages[stage]
+        self.curvature_many([(stage, layer, f, micro)], gate)
+
+    def curvature_many(self, items, gate):
+        """Curvature work items -> SYRK problems, one grouped tcgen05 launch.
+        The first item of a (layer, set) in a cycle overwrites the factor, the
+        others accumulate (the cycle's factor averages its micro-batches)."""
         with torch.cuda.stream(self.kfac_stream):
             if gate is not None:
                 self.kfac_stream.wait_event(gate)
             e0 = self._begin(self.kfac_stream)
-            scale = 1.0 / (self.local_micros[stage] * self.tokens)
-            probs = []
-            for key in ks.keys(f):
-                x = mod.store.get(layer, key, micro)
-                x.record_stream(self.kfac_stream)
-                probs.append((x, ks.factor[(layer, key)], scale, ks.started[(layer, f)]))
-            K.syrk(probs, fill_upper=False)  # one grouped tcgen05 launch per work item
-            ks.started[(layer, f)] = True
+            probs, pending = [], set()
+            for stage, layer, f, micro in items:
+                ks, mod = self.kstate[stage], self.stages[stage]
+                scale = 1.0 / (self.local_micros[stage] * self.tokens)
+                if any((stage, layer, key) in pending for key in ks.keys(f)):
+                    # tiles of one launch are unordered: a factor appears at most
+                    # once per launch (later micro-batches go to the next launch)
+                    K.syrk(probs, fill_upper=False)
+                    probs, pending = [], set()
+                for key in ks.keys(f):
+                    x = mod.store.get(layer, key, micro)
+                    x.record_stream(self.kfac_stream)
+                    probs.append((x, ks.factor[(layer, key)], scale, ks.started[(layer, f)]))
+                    pending.add((stage, layer, key))
+                ks.started[(layer, f)] = True
+            if probs:
+                K.syrk(probs, fill_upper=False)
             self._end("CURV", e0, self.kfac_stream)
 
     def sync_curvature(self, stage, layer, f, group, gate):
@@ -174,26 +193,37 @@ class CudaBackend:
             self._end("SYNC_CURV", e0, self.kfac_stream)
 
     def invert(self, stage, layer, f, gate):
-        ks = self.kstate[stage]
-        slot = (ks.version[(layer, f)] + 1) % 2
+        self.invert_many([(stage, layer, f)], gate)
+
+    def invert_many(self, items, gate):
+        """Inversion work items -> ONE batched damped-inverse call (equal-d
+        factors share launches, independent chains overlap on side streams),
+        into the free slot of each double-buffered inverse."""
+        mats, outs, digs = [], [], []
         with torch.cuda.stream(self.kfac_stream):
             if gate is not None:
                 self.kfac_stream.wait_event(gate)
-            free = ks.slot_free.get((layer, f, slot))
-            if free is not None:  # last precondition that read this slot
-                self.kfac_stream.wait_event(free)
+            for stage, layer, f in items:
+                ks = self.kstate[stage]
+                slot = (ks.version[(layer, f)] + 1) % 2
+                free = ks.slot_free.get((layer, f, slot))
+                if free is not None:  # last precondition that read this slot
+                    self.kfac_stream.wait_event(free)
+                for k in ks.keys(f):
+                    mats.append(ks.factor[(layer, k)])
+                    o = ks.inv[(layer, k, slot)]
+                    outs.append(o.fp32)
+                    digs.append(o.digits)
             e0 = self._begin(self.kfac_stream)
-            keys = ks.keys(f)
-            mats = [ks.factor[(layer, k)] for k in keys]
-            outs = [ks.inv[(layer, k, slot)] for k in keys]
-            K.damped_inverse_batched(mats, self.damping, [o.fp32 for o in outs], [o.digits for o in outs],
-                                     check=False)
+            K.damped_inverse_batched(mats, self.damping, outs, digs, check=False)
             self._end("INV", e0, self.kfac_stream)
             ev = torch.cuda.Event()
             ev.record(self.kfac_stream)
-        ks.version[(layer, f)] += 1
-        ks.started[(layer, f)] = False
-        ks.inv_ready = ev
+        for stage, layer, f in items:
+            ks = self.kstate[stage]
+            ks.version[(layer, f)] += 1
+            ks.started[(layer, f)] = False
+            ks.inv_ready = ev
 
     def broadcast_inverse(self, stage, layer, f, owner, group, gate):
         ks = self.kstate[stage]

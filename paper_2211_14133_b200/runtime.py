@@ -342,19 +342,38 @@ class Executor:
     def run_cycle(self, cycle: int) -> None:
         b, comm = self.backend, self.comm
         fb_done: Dict[int, object] = {}
-        for i, op in enumerate(self.program):
+        prog = self.program
+        i = 0
+        while i < len(prog):
+            op = prog[i]
+            # a run of consecutive Curvature / Inversion items behind the same
+            # gate becomes ONE backend call (one grouped SYRK launch / one
+            # batched inverse whose independent chains overlap)
+            if op.kind in (CURV, INV) and hasattr(b, "curvature_many"):
+                j = i
+                while j < len(prog) and prog[j].kind == op.kind and prog[j].gate == op.gate:
+                    j += 1
+                gate = fb_done.get(op.gate) if op.gate is not None else None
+                items = [(o.stage, o.layer, o.factor, o.micro) for o in prog[i:j]]
+                if op.kind == CURV:
+                    b.curvature_many(items, gate)
+                else:
+                    b.invert_many([it[:3] for it in items], gate)
+                i = j
+                continue
+            i += 1
             if op.kind == F_:
                 x = comm.recv(op.recv, b.act_shape(op.stage, op.micro)) if op.recv else None
                 y = b.forward(op.stage, op.micro, x, capture=(op.step == 0), cycle=cycle)
                 if op.send:
                     comm.send(op.send, y)
-                fb_done[i] = b.mark_compute()
+                fb_done[i - 1] = b.mark_compute()
             elif op.kind == B_:
                 gy = comm.recv(op.recv, b.act_shape(op.stage, op.micro)) if op.recv else None
                 gx = b.backward(op.stage, op.micro, gy, capture=(op.step == 0))
                 if op.send:
                     comm.send(op.send, gx)
-                fb_done[i] = b.mark_compute()
+                fb_done[i - 1] = b.mark_compute()
             else:
                 gate = fb_done.get(op.gate) if op.gate is not None else None
                 if op.kind == CURV:

@@ -1,0 +1,90 @@
+"""PipeFisher trainer on the B200 (engine.py + runtime.py): a small BERT run
+through the single-device inline K-FAC program, with the K-FAC state checked
+against an FP64 torch restatement of the reference formulas on the same
+bf16 tapes (kfac.cpp:125-137, :186-201)."""
+import pytest
+import torch
+
+pytestmark = pytest.mark.gpu
+
+from paper_2211_14133_b200 import schedule as S  # noqa: E402
+from paper_2211_14133_b200.bert import BertConfig  # noqa: E402
+
+
+def small():
+    return BertConfig(hidden=256, ffn=1024, heads=4, layers=2, vocab=512, max_pos=128)
+
+
+def trainer(kfac=True, refresh=2, micro=2):
+    from paper_2211_14133_b200.engine import PipeFisherTrainer
+    cfg = S.PipelineConfig(stages=1, micro_batches=micro, micro_batch_size=4, seq_len=64, layers_per_stage=2)
+    return PipeFisherTrainer(cfg, small(), kfac=kfac, refresh=refresh, damping=0.1, lr=1e-2, seed=3)
+
+
+def rel(a, b):
+    return float((a.double() - b.double()).norm() / b.double().norm())
+
+
+def test_inline_kfac_cycles_run_and_refresh_inverses():
+    t = trainer()
+    ks = t.backend.kstate[0]
+    r0 = t.run_cycle(record=True)
+    assert r0.loss is not None and torch.isfinite(torch.tensor(r0.loss))
+    assert all(v == 0 for v in ks.version.values())  # one refresh per cycle
+    assert 0.0 < r0.util <= 1.0
+    for _ in range(2):
+        r = t.run_cycle()
+    assert all(v == 2 for v in ks.version.values())
+    assert torch.isfinite(torch.tensor(r.loss))
+
+
+def test_curvature_accumulates_micro_batches_like_the_reference():
+    t = trainer(micro=2)
+    b = t.backend
+    for m in range(2):  # step-0 F/B of both micro-batches, tapes captured
+        b.forward(0, m, None, True, 0)
+        b.backward(0, m, None, True)
+    store = b.stages[0].store
+    tapes = {k: v.clone() for k, v in store.tapes.items()}
+    b.curvature_many([(0, l, f, m) for m in range(2) for l in range(2) for f in (0, 1)], None)
+    torch.cuda.synchronize()
+    n = b.tokens * 2
+    ks = b.kstate[0]
+    for l in range(2):
+        for key in ("a_qkv", "a_ffn2", "e_q", "e_ffn1"):
+            want = sum(tapes[(l, key, m)].double() @ tapes[(l, key, m)].double().T for m in range(2)) / n
+            got = torch.tril(ks.factor[(l, key)].double())
+            assert rel(got, torch.tril(want)) < 1e-3, (l, key)
+
+
+def test_inversion_and_fused_update_match_fp64():
+    t = trainer(micro=2)
+    b = t.backend
+    t.run_cycle()  # factors + inverses of cycle 0, weights updated
+    ks = b.kstate[0]
+    lam = 0.1
+    for l, key in ((0, "a_qkv"), (1, "e_ffn1")):
+        A = torch.tril(ks.factor[(l, key)].double())
+        A = A + torch.tril(A, -1).T + lam * torch.eye(A.shape[0], dtype=torch.float64, device=A.device)
+        X = ks.inv[(l, key, 0)].fp32.double()
+        res = (A @ X - torch.eye(A.shape[0], dtype=torch.float64, device=A.device)).abs().max().item()
+        assert res < 1e-5, (l, key, res)
+    # one more step's update through the engine vs FP64 on the same inverses
+    layer = b.stages[0].layers[0]
+    w0 = layer.w["ffn1"].detach().clone()
+    b.forward(0, 0, None, False, 1)
+    b.backward(0, 0, None, False)
+    g = layer.w["ffn1"].grad.detach().clone()
+    ai, bi = ks.inv[(0, "a_ffn1", 0)].fp32.double(), ks.inv[(0, "e_ffn1", 0)].fp32.double()
+    b.precondition(0, 1)
+    torch.cuda.synchronize()
+    want = w0.double() - b.lr * (bi @ g.double() @ ai)
+    got = layer.w["ffn1"].detach().double()
+    assert rel(got - w0.double(), want - w0.double()) < 1e-3
+
+
+def test_plain_pipeline_baseline_has_no_kfac_ops():
+    t = trainer(kfac=False)
+    assert {o.kind for o in t.program} <= {"F", "B", "SYNC_GRAD", "PREC"}
+    r = t.run_cycle(record=True)
+    assert torch.isfinite(torch.tensor(r.loss))
