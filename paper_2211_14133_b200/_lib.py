@@ -12,7 +12,7 @@ import os
 import threading
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "_lib", "libpf_b200.so")
+LIB_PATH = os.environ.get("PF_LIB_PATH") or os.path.join(_HERE, "_lib", "libpf_b200.so")
 
 # pf_status (include/pf_sched.h)
 PF_OK, PF_BAD_SHAPE, PF_NOT_PD, PF_CUDA_ERROR, PF_BAD_ARG, PF_INFEASIBLE = 0, 1, 2, 3, 4, 5

@@ -10,6 +10,8 @@
 #include <cudaTypedefs.h>
 
 #include <algorithm>
+#include <cstdlib>
+#include <utility>
 #include <atomic>
 #include <cstring>
 #include <mutex>
@@ -41,6 +43,35 @@ void check(cudaError_t e, const char* what) {
 void after_launch(const char* what) {
     g_launches.fetch_add(1, std::memory_order_relaxed);
     check(cudaGetLastError(), what);
+}
+
+// Every kernel of this library is launched with programmatic stream
+// serialisation (PDL): it may start while the previous kernel on the stream
+// drains, runs its prologue (barrier init, TMEM alloc, descriptor prefetch),
+// and calls ptx::grid_dep_wait() before touching any global data the previous
+// kernel produced.  PF_NO_PDL=1 launches plainly (A/B measurement).
+bool pdl_enabled() {
+    static const bool on = [] {
+        const char* e = std::getenv("PF_NO_PDL");
+        return !(e && e[0] == '1');
+    }();
+    return on;
+}
+
+template <typename... KArgs, typename... Args>
+void launch(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t st,
+            Args&&... args) {
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = grid;
+    cfg.blockDim = block;
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = st;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = pdl_enabled() ? 1 : 0;
+    check(cudaLaunchKernelEx(&cfg, kernel, std::forward<Args>(args)...), "cudaLaunchKernelEx");
 }
 
 inline int round_up(int x, int m) { return (x + m - 1) / m * m; }
@@ -125,7 +156,7 @@ void launch_slices(const std::vector<SliceReq>& reqs, cudaStream_t st) {
                               r.dst.plane_stride, r.dst.kpad, r.dst.exps, r.dst.sqnorm};
             rows = std::max(rows, r.dst.rows);
         }
-        slice_kernel<<<dim3((rows + 7) / 8, cnt), 256, 0, st>>>(b);
+        launch(slice_kernel, dim3((rows + 7) / 8, cnt), dim3(256), 0, st, b);
         after_launch("slice_kernel");
     }
 }
@@ -210,7 +241,7 @@ void launch_gemms(const std::vector<GemmSpec>& specs, cudaStream_t stream) {
         batch.n_probs = probs;
         batch.total_tiles = tiles;
         if (tiles == 0) continue;
-        kernel<<<tiles, 128, T::kSmemBytes, stream>>>(batch);
+        launch(kernel, dim3(tiles), dim3(128), T::kSmemBytes, stream, batch);
         after_launch("umma_gemm_kernel");
     }
 }
@@ -234,6 +265,8 @@ struct DampBatch {
 // dst = M + damping * I  (lower triangle incl. diagonal; the rest never read)
 __global__ void damp_kernel(const __grid_constant__ DampBatch b) {
     const Damp2D& s = b.e[blockIdx.y];
+    ptx::grid_dep_wait();
+    ptx::grid_dep_launch();
     if (blockIdx.x == 0 && threadIdx.x == 0) *s.info = 0;
     const int64_t total = static_cast<int64_t>(s.d) * s.d;
     for (int64_t idx = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; idx < total;
@@ -247,6 +280,8 @@ __global__ void damp_kernel(const __grid_constant__ DampBatch b) {
 }
 
 __global__ void f32_to_bf16_kernel(const float* x, int64_t n, __nv_bfloat16* out) {
+    ptx::grid_dep_wait();
+    ptx::grid_dep_launch();
     for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < n;
          i += static_cast<int64_t>(gridDim.x) * blockDim.x)
         out[i] = __float2bfloat16_rn(x[i]);
@@ -300,7 +335,7 @@ void launch_leaves(const std::vector<InvWs>& ws, int o, int n, cudaStream_t st) 
             b.e[j] = LeafArgs{at(w.a, w.ld, o, o), at(w.x, w.ld, o, o), at(w.xt, w.ld, o, o),
                               w.info, w.ld, n, o};
         }
-        leaf_chol_inv_kernel<<<cnt, kLeafThreads, kLeafSmemBytes, st>>>(b);
+        launch(leaf_chol_inv_kernel, dim3(cnt), dim3(kLeafThreads), kLeafSmemBytes, st, b);
         after_launch("leaf_chol_inv_kernel");
     }
 }
@@ -427,7 +462,7 @@ void damped_inverse_group(const std::vector<const pf_inverse_problem*>& probs, c
         ws.push_back(w);
     }
     const int blocks = std::min((d * d + 255) / 256, 148 * 8);
-    damp_kernel<<<dim3(blocks, static_cast<unsigned>(probs.size())), 256, 0, st>>>(db);
+    launch(damp_kernel, dim3(blocks, static_cast<unsigned>(probs.size())), dim3(256), 0, st, db);
     after_launch("damp_kernel");
     inverse_rec(ws, 0, d, st);
     // ---- LAUUM: M^-1 = X^T X = XT XT^T  (lower tiles, mirrored)
@@ -607,6 +642,12 @@ using namespace pf;
 extern "C" {
 
 int64_t pf_kernel_launch_count(void) { return g_launches.load(); }
+
+#ifdef PF_GEMM_PROBE
+int pf_gemm_probe_read(long long* out) {
+    return cudaMemcpyFromSymbol(out, pf::g_gemm_probe, sizeof(long long) * 16) == cudaSuccess ? 0 : 3;
+}
+#endif
 
 int pf_device_ok(void) {
     int dev = 0;
@@ -794,8 +835,8 @@ int pf_f32_to_bf16(const float* x, int64_t n, void* out, void* stream) {
         if (n < 0 || !x || !out) throw std::invalid_argument("bad convert");
         const int blocks = static_cast<int>(std::min<int64_t>((n + 255) / 256, 148 * 16));
         if (blocks > 0) {
-            f32_to_bf16_kernel<<<blocks, 256, 0, static_cast<cudaStream_t>(stream)>>>(
-                x, n, static_cast<__nv_bfloat16*>(out));
+            launch(f32_to_bf16_kernel, dim3(blocks), dim3(256), 0, static_cast<cudaStream_t>(stream), x, n,
+                   static_cast<__nv_bfloat16*>(out));
             after_launch("f32_to_bf16_kernel");
         }
         return 0;

@@ -1,24 +1,33 @@
-// Diagonal-block kernel of the damped inverse: for one 128x128 diagonal block
-// A_kk (already holding all trailing updates) compute
-//     L_kk = chol(A_kk)          and          X_kk = L_kk^-1
-// on the SIMT cores, entirely in shared memory, and write X_kk (lower,
-// explicit zeros above) and X_kk^T (upper, zeros below).
+// Diagonal-block kernel of the damped inverse, on the SIMT cores in shared
+// memory (fp32, like LAPACK's SPOTRF/STRTRI block steps):
+//
+//   leaf_chol_inv_kernel   one 128x128 block A_kk (already holding every
+//                          trailing update):  L = chol(A_kk),  X = L^-1;
+//                          writes X (lower, zeros above) and X^T (upper).
 //
 // Follows the reference arithmetic (proj/src/kfac/matrix.cpp:117-153):
 // pivot test `!(diag > 0) || !isfinite(diag)` -> 1-based failing column in
-// *info; L^-1 by forward substitution.  Organisation (B200-first), fp32 like
-// LAPACK's SPOTRF/STRTRI block steps:
-//   * four 32-wide panels; the 32x32 diagonal block of each is factored by
-//     ONE WARP in registers (lane i owns row i).  The column being
-//     eliminated is always register a[0]: after each step the row is rotated
-//     left, so every register index is a compile-time constant while the
-//     32-step loop stays a loop (a fully unrolled version stalled on
-//     instruction fetch: it ran once per panel, ~20K instructions);
-//   * the panel's 32x32 triangular inverse: one lane per column;
-//   * panel solve, trailing update and the off-diagonal blocks of L^-1 are
-//     4x4 register-tiled shared-memory products over all 8 warps.
+// *info; L^-1 by forward substitution.
+//
+// The leaf sits on the sequential chain of the factorisation (d/128 leaves
+// one after another), so it is organised for latency, as a pipeline over four
+// 32-wide panels p with three barrier-separated phases each:
+//   A  warp 0: Cholesky of the 32x32 diagonal block in registers (lane i owns
+//      row i, fully unrolled, the pivot chain runs through a separate
+//      diagonal register so it never waits on the row-update shuffles);
+//      warps 1-7 meanwhile finish the previous panel's trailing update and
+//      compute T_p = L[p, 0:p] X[0:p, 0:p] (block-row forward substitution);
+//   B  panel solve (TRSM), one thread per row below the panel, reading the
+//      transposed diagonal block with float4 broadcasts; the last warp
+//      inverts the diagonal block (X_pp) concurrently;
+//   C  trailing update of the NEXT panel's block column only (all that the
+//      next Cholesky needs) and X[p, 0:p] = -X_pp T_p.
+// All products are 4x4 register tiles fed by float4 shared-memory reads of
+// k-major copies (PT_p = panel transposed, LT / XTd = diagonal blocks
+// transposed), skipping the structurally-zero triangles.
 #pragma once
 
+#include <cfloat>
 #include <climits>
 #include <cstdint>
 
@@ -26,12 +35,36 @@
 
 namespace pf {
 
+#ifdef PF_LEAF_PROBE
+__device__ long long* g_probe;
+#define PF_STAMP(i)                                                      \
+    do {                                                                 \
+        __syncthreads();                                                 \
+        if (threadIdx.x == 0 && blockIdx.x == 0) g_probe[i] = clock64(); \
+    } while (0)
+#else
+#define PF_STAMP(i) \
+    do {            \
+    } while (0)
+#endif
+
 constexpr int kLeaf = 128;
-constexpr int kLeafPitch = 129;  // +1 pad: column walks hit 32 distinct banks
 constexpr int kLeafThreads = 256;
 constexpr int kLeafWarps = kLeafThreads / 32;
 constexpr int kMaxLeafBatch = 32;
-constexpr int kLeafSmemBytes = 2 * kLeaf * kLeafPitch * 4 + kLeaf * 4 + 16;
+// shared-memory layout (floats; every array 16-byte aligned)
+constexpr int kLeafPitch = 129;   // Ls: active trailing matrix (column walks conflict-free)
+constexpr int kXPitch = 132;      // Xs, PT: float4 rows
+constexpr int kSmallPitch = 36;   // LT, XTd: transposed 32x32 diagonal blocks
+constexpr int kTPitch = 100;      // Tb: T_p, 32 x (<= 96)
+constexpr int kLsFloats = kLeaf * kLeafPitch + 4 - (kLeaf * kLeafPitch) % 4;
+constexpr int kXsFloats = kLeaf * kXPitch;
+constexpr int kPTFloats = 32 * kXPitch;
+constexpr int kSmallFloats = 32 * kSmallPitch;
+constexpr int kTbFloats = 32 * kTPitch;
+constexpr int kLeafSmemFloats =
+    kLsFloats + kXsFloats + 3 * kPTFloats + 2 * kSmallFloats + kTbFloats + 64 + kLeaf + 4;
+constexpr int kLeafSmemBytes = kLeafSmemFloats * 4;
 
 struct LeafArgs {
     const float* a;
@@ -47,83 +80,129 @@ struct LeafBatch {
     LeafArgs e[kMaxLeafBatch];
 };
 
-// C[i][j] = alpha * sum_k A[i][k] B[k][j]  (+ C[i][j] if accumulate) over an
-// M x N block (multiples of 4), 4x4 fp32 micro-tiles with strided rows/cols
-// (row ti + r*M/4) so lane-consecutive tiles hit distinct banks.  A(i,k) at
-// a[i*ars + k*aks], B(k,j) at b[k*bks + j*bcs], C(i,j) at c[i*kLeafPitch + j].
-// `lower`: only j <= i is written.  Caller guarantees C does not alias A/B.
-__device__ __forceinline__ void leaf_mm(const float* a, int ars, int aks, const float* b, int bks,
-                                        int bcs, float* c, int M, int N, int K, float alpha,
-                                        bool accumulate, bool lower, int tid, int nthreads) {
-    const int mt = M / 4, nt = N / 4;
-    for (int t = tid; t < mt * nt; t += nthreads) {
-        const int ti = t / nt, tj = t % nt;
-        float acc[4][4];
-#pragma unroll
-        for (int r = 0; r < 4; ++r)
-#pragma unroll
-            for (int q = 0; q < 4; ++q) acc[r][q] = 0.0f;
-        const float* ap = a + ti * ars;
-        const float* bp = b + tj * bcs;
+// acc[u][q] += sum_{k0 <= k < k1} a4(k)[u] * b4(k)[q], a4(k) / b4(k) the
+// float4 at a + k*as / b + k*bs (k ascending, as in the reference loops).
+__device__ __forceinline__ void outer4(float (&acc)[4][4], const float* a, int as, const float* b,
+                                       int bs, int k0, int k1) {
 #pragma unroll 4
-        for (int k = 0; k < K; ++k) {
-            float av[4], bv[4];
+    for (int k = k0; k < k1; ++k) {
+        const float4 av = *reinterpret_cast<const float4*>(a + k * as);
+        const float4 bv = *reinterpret_cast<const float4*>(b + k * bs);
+        const float ar[4] = {av.x, av.y, av.z, av.w};
+        const float br[4] = {bv.x, bv.y, bv.z, bv.w};
 #pragma unroll
-            for (int r = 0; r < 4; ++r) av[r] = ap[r * mt * ars + k * aks];
+        for (int u = 0; u < 4; ++u)
 #pragma unroll
-            for (int q = 0; q < 4; ++q) bv[q] = bp[k * bks + q * nt * bcs];
-#pragma unroll
-            for (int r = 0; r < 4; ++r)
-#pragma unroll
-                for (int q = 0; q < 4; ++q) acc[r][q] = fmaf(av[r], bv[q], acc[r][q]);
-        }
-#pragma unroll
-        for (int r = 0; r < 4; ++r)
-#pragma unroll
-            for (int q = 0; q < 4; ++q) {
-                const int i = ti + r * mt, j = tj + q * nt;
-                if (lower && j > i) continue;
-                float* dst = c + i * kLeafPitch + j;
-                *dst = accumulate ? fmaf(alpha, acc[r][q], *dst) : alpha * acc[r][q];
-            }
+            for (int q = 0; q < 4; ++q) acc[u][q] = fmaf(ar[u], br[q], acc[u][q]);
     }
 }
 
-// One warp: Cholesky of the 32x32 block at (c0, c0) of Ls (in place, zeros
-// above the diagonal), then its inverse into Xs (zeros above the diagonal).
-__device__ __forceinline__ void panel_chol_inv32(float* Ls, float* Xs, float* rdiag, int c0,
-                                                 int col_base, int n, int* bad) {
+__device__ __forceinline__ void zero4x4(float (&acc)[4][4]) {
+#pragma unroll
+    for (int u = 0; u < 4; ++u)
+#pragma unroll
+        for (int q = 0; q < 4; ++q) acc[u][q] = 0.0f;
+}
+
+// t -> (i, j) with i >= j, t = i(i+1)/2 + j
+__device__ __forceinline__ void lower_pair(int t, int& i, int& j) {
+    int m = static_cast<int>((sqrtf(8.0f * static_cast<float>(t) + 1.0f) - 1.0f) * 0.5f);
+    while ((m + 1) * (m + 2) / 2 <= t) ++m;
+    while (m * (m + 1) / 2 > t) --m;
+    i = m;
+    j = t - m * (m + 1) / 2;
+}
+
+// ---- phase A, warp 0: Cholesky of the 32x32 diagonal block at (c0, c0) of Ls.
+// Writes LT[j][i] = L[i][j] (zeros above the diagonal) and rdiag = 1/L[k][k].
+// Lane i owns row i; entries above the diagonal pick up garbage in registers
+// but never feed a value that is kept.
+__device__ __forceinline__ float rsqrt_ftz(float x) {
+    float y;
+    asm("rsqrt.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+    return y;
+}
+
+__device__ __forceinline__ void chol32(const float* Ls, float* LT, float* rdiag, float* lbuf, int c0, int n,
+                                       int col_base, int* bad) {
     const int lane = threadIdx.x & 31;
-    float* row = Ls + (c0 + lane) * kLeafPitch + c0;
+    const float* row = Ls + (c0 + lane) * kLeafPitch + c0;
     float a[32];
 #pragma unroll
     for (int j = 0; j < 32; ++j) a[j] = row[j];
-#pragma unroll 1
+    float dii = row[lane];  // == a[lane], kept apart so the pivot chain is short
+    int badcol = INT_MAX;
+#pragma unroll
     for (int k = 0; k < 32; ++k) {
-        // a[0] holds column k of this lane's row (rotated k times)
-        float piv = __shfl_sync(0xffffffffu, a[0], k);
-        if (!(piv > 0.0f) || !isfinite(piv)) {
-            if (lane == 0 && c0 + k < n) *bad = min(*bad, col_base + c0 + k + 1);  // one warp: no race
-            piv = 1.0f;  // keep going; the caller reports the failure
-        }
-        const float rl = rsqrtf(piv);
-        const float l = lane > k ? a[0] * rl : (lane == k ? piv * rl : 0.0f);
-        row[k] = l;  // L[lane][c0+k] (0 above the diagonal)
+        const float piv = __shfl_sync(0xffffffffu, dii, k);  // warp-uniform
+#ifdef PF_CHOL_OLDPIV
+        const bool ok = piv > 0.0f && piv <= FLT_MAX;
+        const float pv = ok ? piv : 1.0f;
+        const float rl = rsqrtf(pv);
+#else
+        // a failed pivot (<= 0, inf, NaN) is recorded and then propagates NaN /
+        // inf through the block; the caller raises on info != 0
+        const bool ok = piv > 0.0f && piv <= FLT_MAX;
+        const float pv = piv;
+        const float rl = rsqrt_ftz(piv);
+#endif
+        if (!ok && c0 + k < n && badcol == INT_MAX) badcol = col_base + c0 + k + 1;
+        const float l = lane > k ? a[k] * rl : (lane == k ? pv * rl : 0.0f);
+        a[k] = l;
+        dii = fmaf(-l, l, dii);
         if (lane == k) rdiag[c0 + k] = rl;
-        // all shuffles first (independent), then the dependent FMAs
-        float lj[32];
+#ifdef PF_CHOL_SHFL
 #pragma unroll
-        for (int j = 1; j < 32; ++j) lj[j] = __shfl_sync(0xffffffffu, l, (k + j) & 31);
+        for (int j = k + 1; j < 32; ++j) a[j] = fmaf(-l, __shfl_sync(0xffffffffu, l, j), a[j]);
+#else
+        // broadcast l through shared memory (double-buffered by step parity)
+        float* lb = lbuf + 32 * (k & 1);
+        lb[lane] = l;
+        __syncwarp();
 #pragma unroll
-        for (int j = 1; j < 32; ++j)
-            if (lane >= k + j) a[j] = fmaf(-l, lj[j], a[j]);
+        for (int q4 = (k + 1) / 4; q4 < 8; ++q4) {
+            const float4 v = *reinterpret_cast<const float4*>(lb + 4 * q4);
+            const float lv[4] = {v.x, v.y, v.z, v.w};
 #pragma unroll
-        for (int j = 0; j < 31; ++j) a[j] = a[j + 1];
-        a[31] = 0.0f;
+            for (int e = 0; e < 4; ++e)
+                if (4 * q4 + e > k) a[4 * q4 + e] = fmaf(-l, lv[e], a[4 * q4 + e]);
+        }
+#endif
     }
-    __syncwarp();
-    // column `lane` of L^-1 by forward substitution (reference matrix.cpp:145-153),
-    // column-oriented: every index is a compile-time constant
+    if (lane == 0 && badcol != INT_MAX) *bad = min(*bad, badcol);
+#pragma unroll
+    for (int j = 0; j < 32; ++j) LT[j * kSmallPitch + lane] = j <= lane ? a[j] : 0.0f;
+}
+
+// ---- phase B: row r of the panel solve  L[r, p] = A[r, p] L_pp^-T  by
+// forward substitution (x_j final -> eliminate it from the later entries;
+// reference matrix.cpp order), result stored transposed: PTp[k][r].
+__device__ __forceinline__ void trsm_row(const float* Ls, const float* LT, const float* rdiag, float* PTp,
+                                         int c0, int r) {
+    const float* row = Ls + r * kLeafPitch + c0;
+    float x[32];
+#pragma unroll
+    for (int j = 0; j < 32; ++j) x[j] = row[j];
+#pragma unroll
+    for (int j = 0; j < 32; ++j) {
+        x[j] *= rdiag[c0 + j];
+#pragma unroll
+        for (int q4 = (j + 1) / 4; q4 < 8; ++q4) {
+            const float4 v = *reinterpret_cast<const float4*>(LT + j * kSmallPitch + 4 * q4);
+            const float lv[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+            for (int e = 0; e < 4; ++e)
+                if (4 * q4 + e > j) x[4 * q4 + e] = fmaf(-x[j], lv[e], x[4 * q4 + e]);
+        }
+    }
+#pragma unroll
+    for (int k = 0; k < 32; ++k) PTp[k * kXPitch + r] = x[k];
+}
+
+// ---- phase B, one warp: X_pp = L_pp^-1 (lane c computes column c, reference
+// matrix.cpp:145-153); into Xs (zeros above the diagonal) and XTd[c][i] = X[i][c].
+__device__ __forceinline__ void inv32(const float* LT, const float* rdiag, float* Xs, float* XTd, int c0) {
+    const int lane = threadIdx.x & 31;
     float x[32];
 #pragma unroll
     for (int i = 0; i < 32; ++i) x[i] = (i == lane) ? 1.0f : 0.0f;
@@ -131,28 +210,70 @@ __device__ __forceinline__ void panel_chol_inv32(float* Ls, float* Xs, float* rd
     for (int i = 0; i < 32; ++i) {
         x[i] *= rdiag[c0 + i];
 #pragma unroll
-        for (int r = i + 1; r < 32; ++r) x[r] = fmaf(-Ls[(c0 + r) * kLeafPitch + c0 + i], x[i], x[r]);
+        for (int q4 = (i + 1) / 4; q4 < 8; ++q4) {
+            const float4 v = *reinterpret_cast<const float4*>(LT + i * kSmallPitch + 4 * q4);
+            const float lv[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+            for (int e = 0; e < 4; ++e)
+                if (4 * q4 + e > i) x[4 * q4 + e] = fmaf(-lv[e], x[i], x[4 * q4 + e]);
+        }
     }
 #pragma unroll
-    for (int i = 0; i < 32; ++i) Xs[(c0 + i) * kLeafPitch + c0 + lane] = x[i];
+    for (int i = 0; i < 32; ++i) Xs[(c0 + i) * kXPitch + c0 + lane] = x[i];
+#pragma unroll
+    for (int i = 0; i < 32; i += 4)
+        *reinterpret_cast<float4*>(XTd + lane * kSmallPitch + i) = make_float4(x[i], x[i + 1], x[i + 2], x[i + 3]);
 }
 
-__global__ void __launch_bounds__(kLeafThreads, 1) leaf_chol_inv_kernel(const __grid_constant__ LeafBatch batch) {
-    extern __shared__ float leaf_smem[];
-    float* Ls = leaf_smem;
-    float* Xs = leaf_smem + kLeaf * kLeafPitch;
-    float* rdiag = Xs + kLeaf * kLeafPitch;  // 1 / L[k][k]
-    int* bad = reinterpret_cast<int*>(rdiag + kLeaf);
-    const LeafArgs& A = batch.e[blockIdx.x];
-    const int n = A.n;
-    const int tid = threadIdx.x;
-    const int warp = tid >> 5;
-    const int lane = tid & 31;
+// trailing-update tile: Ls[r][c] -= sum_k L[r][k] L[c][k] over panel PTp, for
+// the 4x4 tile at (r0, cc), lower part only
+__device__ __forceinline__ void trail_tile(float* Ls, const float* PTp, int r0, int cc) {
+    float acc[4][4];
+    zero4x4(acc);
+    outer4(acc, PTp + r0, kXPitch, PTp + cc, kXPitch, 0, 32);
+#pragma unroll
+    for (int u = 0; u < 4; ++u)
+#pragma unroll
+        for (int q = 0; q < 4; ++q)
+            if (cc + q <= r0 + u) {
+                float* d = Ls + (r0 + u) * kLeafPitch + cc + q;
+                *d = fmaf(-1.0f, acc[u][q], *d);
+            }
+}
 
-    if (tid == 0) *bad = INT_MAX;
-    // load the lower triangle of A; pad beyond n with the identity.  Full
-    // blocks (n == 128, 16-byte aligned rows) use float4 loads, all in flight.
-    const bool vec = n == kLeaf && (A.ld % 4 == 0) && ((reinterpret_cast<uintptr_t>(A.a) & 15) == 0);
+// T_p tile (ti in [0,8), tj in [0, 8p)): T[i][j] = sum_{k} L[32p+i][k] X[k][j],
+// k from 4tj (X is lower triangular) to 32p, L rows read from the panels PT_q.
+__device__ __forceinline__ void tprod_tile(const float* PT, const float* Xs, float* Tb, int p, int ti, int tj) {
+    float acc[4][4];
+    zero4x4(acc);
+    const int kstart = 4 * tj;
+    for (int q = kstart / 32; q < p; ++q) {
+        const int k0 = max(kstart - 32 * q, 0);
+        outer4(acc, PT + q * kPTFloats + 32 * p + 4 * ti, kXPitch, Xs + (32 * q) * kXPitch + 4 * tj, kXPitch,
+               k0, 32);
+    }
+#pragma unroll
+    for (int u = 0; u < 4; ++u)
+        *reinterpret_cast<float4*>(Tb + (4 * ti + u) * kTPitch + 4 * tj) =
+            make_float4(acc[u][0], acc[u][1], acc[u][2], acc[u][3]);
+}
+
+// X[32p+i][j] = -sum_{k <= i} X_pp[i][k] T[k][j]  for the 4x4 tile (ti, tj)
+__device__ __forceinline__ void xprod_tile(const float* XTd, const float* Tb, float* Xs, int p, int ti, int tj) {
+    float acc[4][4];
+    zero4x4(acc);
+    outer4(acc, XTd + 4 * ti, kSmallPitch, Tb + 4 * tj, kTPitch, 0, 4 * ti + 4);
+#pragma unroll
+    for (int u = 0; u < 4; ++u)
+        *reinterpret_cast<float4*>(Xs + (32 * p + 4 * ti + u) * kXPitch + 4 * tj) =
+            make_float4(-acc[u][0], -acc[u][1], -acc[u][2], -acc[u][3]);
+}
+
+// ---- global <-> shared (256 threads)
+// dst = lower triangle of the n x n block at src (zeros above, identity beyond n)
+__device__ __forceinline__ void load_lower(float* dst, const float* src, int ld, int n) {
+    const int tid = threadIdx.x;
+    const bool vec = n == kLeaf && (ld % 4 == 0) && ((reinterpret_cast<uintptr_t>(src) & 15) == 0);
     if (vec) {
         constexpr int kPer = kLeaf * kLeaf / 4 / kLeafThreads;  // 16 float4 per thread
         float4 v[kPer];
@@ -160,115 +281,159 @@ __global__ void __launch_bounds__(kLeafThreads, 1) leaf_chol_inv_kernel(const __
         for (int q = 0; q < kPer; ++q) {
             const int idx = tid + q * kLeafThreads;
             const int r = idx / (kLeaf / 4), c = 4 * (idx % (kLeaf / 4));
-            v[q] = (c <= r) ? *reinterpret_cast<const float4*>(A.a + (size_t)r * A.ld + c)
+            v[q] = (c <= r) ? *reinterpret_cast<const float4*>(src + (size_t)r * ld + c)
                             : make_float4(0.f, 0.f, 0.f, 0.f);
         }
 #pragma unroll
         for (int q = 0; q < kPer; ++q) {
             const int idx = tid + q * kLeafThreads;
             const int r = idx / (kLeaf / 4), c = 4 * (idx % (kLeaf / 4));
-            float* dst = Ls + r * kLeafPitch + c;
-            dst[0] = c <= r ? v[q].x : 0.f;
-            dst[1] = c + 1 <= r ? v[q].y : 0.f;
-            dst[2] = c + 2 <= r ? v[q].z : 0.f;
-            dst[3] = c + 3 <= r ? v[q].w : 0.f;
-            float* xz = Xs + r * kLeafPitch + c;
-            xz[0] = xz[1] = xz[2] = xz[3] = 0.f;
+            float* d = dst + r * kLeafPitch + c;
+            d[0] = c <= r ? v[q].x : 0.f;
+            d[1] = c + 1 <= r ? v[q].y : 0.f;
+            d[2] = c + 2 <= r ? v[q].z : 0.f;
+            d[3] = c + 3 <= r ? v[q].w : 0.f;
         }
     } else {
         for (int idx = tid; idx < kLeaf * kLeaf; idx += kLeafThreads) {
             const int r = idx / kLeaf, c = idx % kLeaf;
             float v;
             if (r < n && c < n)
-                v = (c <= r) ? A.a[(size_t)r * A.ld + c] : 0.0f;
+                v = (c <= r) ? src[(size_t)r * ld + c] : 0.0f;
             else
                 v = (r == c) ? 1.0f : 0.0f;
-            Ls[r * kLeafPitch + c] = v;
-            Xs[r * kLeafPitch + c] = 0.0f;
+            dst[r * kLeafPitch + c] = v;
         }
     }
-    __syncthreads();
+}
 
-    // ---- blocked right-looking Cholesky, 32-wide panels
-    for (int p = 0; p < 4; ++p) {
-        const int c0 = 32 * p;
-        if (warp == 0) panel_chol_inv32(Ls, Xs, rdiag, c0, A.col0, n, bad);
-        __syncthreads();
-        if (p == 3) break;
-        // panel solve  L[i, p] = A[i, p] Linv_pp^T  (in place; a warp owns a row
-        // and reads all of it before writing it)
-        for (int i = c0 + 32 + warp; i < kLeaf; i += kLeafWarps) {
-            float s0 = 0.0f, s1 = 0.0f;
-#pragma unroll
-            for (int k = 0; k < 32; k += 2) {
-                s0 = fmaf(Ls[i * kLeafPitch + c0 + k], Xs[(c0 + lane) * kLeafPitch + c0 + k], s0);
-                s1 = fmaf(Ls[i * kLeafPitch + c0 + k + 1], Xs[(c0 + lane) * kLeafPitch + c0 + k + 1], s1);
-            }
-            __syncwarp();
-            Ls[i * kLeafPitch + c0 + lane] = s0 + s1;
-        }
-        __syncthreads();
-        // trailing update  A[i, j] -= L[i, p] L[j, p]^T   (lower part)
-        const int m = kLeaf - c0 - 32;
-        const float* lp = Ls + (c0 + 32) * kLeafPitch + c0;
-        leaf_mm(lp, kLeafPitch, 1, lp, 1, kLeafPitch, Ls + (c0 + 32) * kLeafPitch + c0 + 32, m, m, 32,
-                -1.0f, true, true, tid, kLeafThreads);
-        __syncthreads();
+// zero the strictly-upper 32x32 blocks of Xs (never written otherwise)
+__device__ __forceinline__ void zero_upper_blocks(float* Xs) {
+    for (int idx = threadIdx.x; idx < kLeaf * kLeaf / 4; idx += kLeafThreads) {
+        const int r = idx / (kLeaf / 4), c = 4 * (idx % (kLeaf / 4));
+        if (c >= 32 * (r / 32 + 1))
+            *reinterpret_cast<float4*>(Xs + r * kXPitch + c) = make_float4(0.f, 0.f, 0.f, 0.f);
     }
+}
 
-    // ---- off-diagonal 32-blocks of L^-1, by block diagonal:
-    //   X[bi,bj] = -Linv_bi * ( sum_{k=bj}^{bi-1} L[bi,k] X[k,bj] )
-    // The temporary sum T(bi,bj) is staged in the (unused) upper block (bj,bi) of Ls.
-    for (int dgap = 1; dgap < 4; ++dgap) {
-        const int pairs = 4 - dgap;
-        // one 64-thread group per block pair (64 micro-tiles of 4x4 each)
-        const int q = tid / 64, qt = tid % 64;
-        const int bj = q, bi = q + dgap;
-        if (q < pairs)  // T = L[bi, bj..bi-1] * X[bj..bi-1, bj]
-            leaf_mm(Ls + (32 * bi) * kLeafPitch + 32 * bj, kLeafPitch, 1,
-                    Xs + (32 * bj) * kLeafPitch + 32 * bj, kLeafPitch, 1,
-                    Ls + (32 * bj) * kLeafPitch + 32 * bi, 32, 32, 32 * dgap, 1.0f, false, false,
-                    qt, 64);
-        __syncthreads();
-        if (q < pairs)  // X[bi, bj] = -Linv_bi T
-            leaf_mm(Xs + (32 * bi) * kLeafPitch + 32 * bi, kLeafPitch, 1,
-                    Ls + (32 * bj) * kLeafPitch + 32 * bi, kLeafPitch, 1,
-                    Xs + (32 * bi) * kLeafPitch + 32 * bj, 32, 32, 32, -1.0f, false, false, qt, 64);
-        __syncthreads();
-    }
-
-    // ---- store X (lower, zeros above) and X^T (upper, zeros below)
-    if (vec && (reinterpret_cast<uintptr_t>(A.x) & 15) == 0 && (reinterpret_cast<uintptr_t>(A.xt) & 15) == 0) {
+// x = X (lower, zeros above) and xt = X^T for the n x n block
+__device__ __forceinline__ void store_x(const float* Xs, float* x, float* xt, int ld, int n) {
+    const int tid = threadIdx.x;
+    const bool vec = n == kLeaf && (ld % 4 == 0) && ((reinterpret_cast<uintptr_t>(x) & 15) == 0) &&
+                     ((reinterpret_cast<uintptr_t>(xt) & 15) == 0);
+    if (vec) {
         for (int idx = tid; idx < kLeaf * kLeaf / 4; idx += kLeafThreads) {
             const int r = idx / (kLeaf / 4), c = 4 * (idx % (kLeaf / 4));
-            float4 lo, up;
-            lo.x = c <= r ? Xs[r * kLeafPitch + c] : 0.f;
-            lo.y = c + 1 <= r ? Xs[r * kLeafPitch + c + 1] : 0.f;
-            lo.z = c + 2 <= r ? Xs[r * kLeafPitch + c + 2] : 0.f;
-            lo.w = c + 3 <= r ? Xs[r * kLeafPitch + c + 3] : 0.f;
-            up.x = r <= c ? Xs[c * kLeafPitch + r] : 0.f;
-            up.y = r <= c + 1 ? Xs[(c + 1) * kLeafPitch + r] : 0.f;
-            up.z = r <= c + 2 ? Xs[(c + 2) * kLeafPitch + r] : 0.f;
-            up.w = r <= c + 3 ? Xs[(c + 3) * kLeafPitch + r] : 0.f;
-            *reinterpret_cast<float4*>(A.x + (size_t)r * A.ld + c) = lo;
-            *reinterpret_cast<float4*>(A.xt + (size_t)r * A.ld + c) = up;
+            *reinterpret_cast<float4*>(x + (size_t)r * ld + c) =
+                *reinterpret_cast<const float4*>(Xs + r * kXPitch + c);
+        }
+        for (int idx = tid; idx < kLeaf * kLeaf / 4; idx += kLeafThreads) {
+            const int r = idx % kLeaf, c = 4 * (idx / kLeaf);  // lanes: consecutive r (conflict-free)
+            *reinterpret_cast<float4*>(xt + (size_t)r * ld + c) =
+                make_float4(Xs[c * kXPitch + r], Xs[(c + 1) * kXPitch + r], Xs[(c + 2) * kXPitch + r],
+                            Xs[(c + 3) * kXPitch + r]);
         }
     } else {
         for (int idx = tid; idx < n * n; idx += kLeafThreads) {
             const int r = idx / n, c = idx % n;
-            A.x[(size_t)r * A.ld + c] = (c <= r) ? Xs[r * kLeafPitch + c] : 0.0f;
-            A.xt[(size_t)r * A.ld + c] = (r <= c) ? Xs[c * kLeafPitch + r] : 0.0f;
+            x[(size_t)r * ld + c] = Xs[r * kXPitch + c];
+            xt[(size_t)r * ld + c] = Xs[c * kXPitch + r];
         }
     }
-    if (tid == 0 && *bad != INT_MAX) {
-        // keep the smallest failing column across blocks (0 = success)
-        int old = *A.info;
-        while (old == 0 || *bad < old) {
-            const int seen = atomicCAS(A.info, old, *bad);
-            if (seen == old) break;
-            old = seen;
-        }
+}
+
+__device__ __forceinline__ void report_bad(int* info, int bad) {
+    if (bad == INT_MAX) return;
+    // keep the smallest failing column across blocks (0 = success)
+    int old = *info;
+    while (old == 0 || bad < old) {
+        const int seen = atomicCAS(info, old, bad);
+        if (seen == old) break;
+        old = seen;
     }
+}
+
+__global__ void __launch_bounds__(kLeafThreads, 1) leaf_chol_inv_kernel(const __grid_constant__ LeafBatch batch) {
+    extern __shared__ __align__(16) float leaf_smem[];
+    float* Ls = leaf_smem;
+    float* Xs = Ls + kLsFloats;
+    float* PT = Xs + kXsFloats;  // panels 0..2, transposed
+    float* LT = PT + 3 * kPTFloats;
+    float* XTd = LT + kSmallFloats;
+    float* Tb = XTd + kSmallFloats;
+    float* lbuf = Tb + kTbFloats;  // chol32 broadcast buffer, 2 x 32
+    float* rdiag = lbuf + 64;
+    int* bad = reinterpret_cast<int*>(rdiag + kLeaf);
+    const LeafArgs& A = batch.e[blockIdx.x];
+    const int tid = threadIdx.x;
+    const int warp = tid >> 5;
+
+    PF_STAMP(0);
+    if (tid == 0) *bad = INT_MAX;
+    zero_upper_blocks(Xs);
+    PF_STAMP(1);
+    ptx::grid_dep_wait();  // PDL: A is produced by the previous launch
+    load_lower(Ls, A.a, A.ld, A.n);
+    __syncthreads();
+    PF_STAMP(2);
+
+    for (int p = 0; p < 4; ++p) {
+        const int c0 = 32 * p;
+        // ---- A: chol(p) || rest of U(p-1) + T_p
+        if (warp == 0) {
+            chol32(Ls, LT, rdiag, lbuf, c0, A.n, A.col0, bad);
+        } else if (p > 0) {
+            const int base = 8 * (p + 1), m = 32 - base;  // tile rows/cols [base, 32), lower
+            const int nrest = m * (m + 1) / 2;
+            const int ntp = 64 * p;
+            for (int t = tid - 32; t < nrest + ntp; t += kLeafThreads - 32) {
+                if (t < nrest) {
+                    int i, j;
+                    lower_pair(t, i, j);
+                    trail_tile(Ls, PT + (p - 1) * kPTFloats, 4 * (base + i), 4 * (base + j));
+                } else {
+                    const int u = t - nrest;
+                    tprod_tile(PT, Xs, Tb, p, u / (8 * p), u % (8 * p));
+                }
+            }
+        }
+        __syncthreads();
+        PF_STAMP(3 + 3 * p);
+        if (p == 3) break;
+        // ---- B: TRSM of the rows below || X_pp
+        const int below = kLeaf - c0 - 32;
+        if (tid < below) trsm_row(Ls, LT, rdiag, PT + p * kPTFloats, c0, c0 + 32 + tid);
+        if (warp == kLeafWarps - 1) inv32(LT, rdiag, Xs, XTd, c0);
+        __syncthreads();
+        PF_STAMP(4 + 3 * p);
+        // ---- C: U(p) on block column p+1 || X[p, 0:p] = -X_pp T_p
+        {
+            const int base = 8 * (p + 1), rows = 32 - base;
+            const int nu = rows * 8, nx = 64 * p;
+            for (int t = tid; t < nu + nx; t += kLeafThreads) {
+                if (t < nu) {
+                    const int tr = base + t / 8, tc = base + t % 8;
+                    if (tc <= tr) trail_tile(Ls, PT + p * kPTFloats, 4 * tr, 4 * tc);
+                } else {
+                    const int u = t - nu;
+                    xprod_tile(XTd, Tb, Xs, p, u / (8 * p), u % (8 * p));
+                }
+            }
+        }
+        __syncthreads();
+        PF_STAMP(5 + 3 * p);
+    }
+    // ---- tail: X_33, then X[3, 0:3] = -X_33 T_3
+    if (warp == 0) inv32(LT, rdiag, Xs, XTd, 96);
+    __syncthreads();
+    PF_STAMP(13);
+    for (int t = tid; t < 192; t += kLeafThreads) xprod_tile(XTd, Tb, Xs, 3, t / 24, t % 24);
+    __syncthreads();
+    PF_STAMP(14);
+    ptx::grid_dep_launch();
+    store_x(Xs, A.x, A.xt, A.ld, A.n);
+    PF_STAMP(19);
+    if (tid == 0) report_bad(A.info, *bad);
 }
 
 }  // namespace pf

@@ -31,6 +31,15 @@ __device__ __forceinline__ bool elect_one() {
 }
 
 // ---------------------------------------------------------------- mbarrier
+// Programmatic dependent launch (PDL).  Kernels launched with the
+// programmatic-stream-serialization attribute run their prologue while the
+// previous kernel drains; `grid_dep_wait` blocks until that kernel has
+// completed and its writes are visible.  Both are no-ops without the attribute.
+__device__ __forceinline__ void grid_dep_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void grid_dep_launch() {
+    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+}
+
 __device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
     asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
 }

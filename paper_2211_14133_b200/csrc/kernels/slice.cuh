@@ -17,6 +17,8 @@
 // neither read nor written: the GEMM's k-range never loads them.
 #pragma once
 
+#include "ptx.cuh"
+
 #include <cstdint>
 
 namespace pf {
@@ -74,6 +76,8 @@ __global__ void __launch_bounds__(256) slice_kernel(const __grid_constant__ Slic
     const SliceJob& J = b.j[blockIdx.y];
     const int r = blockIdx.x * 8 + (threadIdx.x >> 5);
     const int lane = threadIdx.x & 31;
+    ptx::grid_dep_wait();  // PDL: the rows are produced by the previous launch
+    ptx::grid_dep_launch();
     if (r >= J.rows) return;
     int lo, hi;
     valid_range(J, r, lo, hi);

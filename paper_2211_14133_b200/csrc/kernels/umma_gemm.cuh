@@ -32,6 +32,18 @@
 
 namespace pf {
 
+#ifdef PF_GEMM_PROBE
+__device__ long long g_gemm_probe[16];
+#define PF_GSTAMP(i, cond)                                          \
+    do {                                                            \
+        if ((cond) && blockIdx.x == 0) g_gemm_probe[i] = clock64(); \
+    } while (0)
+#else
+#define PF_GSTAMP(i, cond) \
+    do {                   \
+    } while (0)
+#endif
+
 constexpr int kTile = 128;
 constexpr int kMaxMaps = 96;
 constexpr int kMaxProbs = 16;
@@ -143,10 +155,8 @@ __global__ void __launch_bounds__(128, GemmTraits<kFmt>::kMinBlocks)
     const int warp = threadIdx.x >> 5;
     const uint32_t lane = threadIdx.x & 31;
 
-    if constexpr (kFmt == kOZ8) {
-        const int c = tn * kTile + static_cast<int>(threadIdx.x);
-        col_scale[threadIdx.x] = c < P.cols ? ptx::pow2f(P.b_exp[c]) : 0.0f;
-    }
+    PF_GSTAMP(0, threadIdx.x == 0);
+    // prologue (overlaps the previous kernel's tail under PDL)
     if (threadIdx.x == 0) {
         for (int s = 0; s < kStages; ++s) {
             ptx::mbar_init(&full[s], 1);
@@ -156,10 +166,22 @@ __global__ void __launch_bounds__(128, GemmTraits<kFmt>::kMinBlocks)
         ptx::fence_barrier_init();
     }
     if (warp == 0) ptx::tmem_alloc<T::kTmemCols>(tmem_slot);
+    if (warp == 0 && lane == 0) {
+        for (int pl = 0; pl < T::kPlanes; ++pl) {
+            ptx::prefetch_tmap(&batch.maps[P.a_map + pl]);
+            ptx::prefetch_tmap(&batch.maps[P.b_map + pl]);
+        }
+    }
+    ptx::grid_dep_wait();  // operands, scales and C come from earlier launches
+    if constexpr (kFmt == kOZ8) {
+        const int c = tn * kTile + static_cast<int>(threadIdx.x);
+        col_scale[threadIdx.x] = c < P.cols ? ptx::pow2f(P.b_exp[c]) : 0.0f;
+    }
     ptx::tc_fence_before();
     __syncthreads();
     ptx::tc_fence_after();
     const uint32_t tmem = *tmem_slot;
+    PF_GSTAMP(1, threadIdx.x == 0);
 
     auto a_plane = [&](int s, int pl) { return smem + s * T::kStageBytes + pl * T::kPlaneBytes; };
     auto b_plane = [&](int s, int pl) {
@@ -168,10 +190,6 @@ __global__ void __launch_bounds__(128, GemmTraits<kFmt>::kMinBlocks)
 
     if (warp == 0 && lane == 0) {
         // ---------------- TMA producer
-        for (int pl = 0; pl < T::kPlanes; ++pl) {
-            ptx::prefetch_tmap(&batch.maps[P.a_map + pl]);
-            ptx::prefetch_tmap(&batch.maps[P.b_map + pl]);
-        }
         int s = 0;
         uint32_t ph = 0;
         for (int kb = kb0; kb < kb1; ++kb) {
@@ -195,6 +213,7 @@ __global__ void __launch_bounds__(128, GemmTraits<kFmt>::kMinBlocks)
         for (int kb = kb0; kb < kb1; ++kb) {
             ptx::mbar_wait(&full[s], ph);
             ptx::tc_fence_after();
+            PF_GSTAMP(2, kb == kb0);
 #pragma unroll
             for (int ks = 0; ks < T::kKSteps; ++ks) {
                 const uint32_t off = ks * 32;  // 32 B per UMMA k-step
@@ -224,6 +243,7 @@ __global__ void __launch_bounds__(128, GemmTraits<kFmt>::kMinBlocks)
             }
         }
         ptx::umma_commit(done);
+        PF_GSTAMP(3, true);
     }
     __syncwarp();
 
@@ -233,6 +253,8 @@ __global__ void __launch_bounds__(128, GemmTraits<kFmt>::kMinBlocks)
         ptx::mbar_wait(done, 0);
         ptx::tc_fence_after();
     }
+    PF_GSTAMP(4, threadIdx.x == 0);
+    ptx::grid_dep_launch();  // main loop done: let the next launch start its prologue
     __syncwarp();
     const int r = tm * kTile + warp * 32 + static_cast<int>(lane);
     const bool row_ok = r < P.rows;
@@ -240,8 +262,11 @@ __global__ void __launch_bounds__(128, GemmTraits<kFmt>::kMinBlocks)
     const bool mirror = (f & EPI_MIRROR) && tm != tn;
     const uint32_t lane_base = tmem + (static_cast<uint32_t>(warp * 32) << 16);
     float row_scale = 1.0f;
+    const bool exact_diag = (f & EPI_EXACT_DIAG) && tm == tn && row_ok;
+    float diag_exact = 0.0f;
     if constexpr (kFmt == kOZ8) {
         if (row_ok) row_scale = P.alpha * ptx::pow2f(P.a_exp[r]);
+        if (exact_diag) diag_exact = static_cast<float>(P.a_sqnorm[r] * 0x1p14);
     }
 #pragma unroll 1
     for (int chunk = 0; chunk < kTile / 16; ++chunk) {
@@ -263,7 +288,7 @@ __global__ void __launch_bounds__(128, GemmTraits<kFmt>::kMinBlocks)
 #pragma unroll
                     for (int j = 0; j < 16; ++j) raw[g][j] = 0u;
             }
-            const bool diag_chunk = (f & EPI_EXACT_DIAG) && tm == tn && row_ok && r >= c0 && r < c0 + 16;
+            const bool diag_chunk = exact_diag && r >= c0 && r < c0 + 16;
 #pragma unroll
             for (int j = 0; j < 16; ++j) {
                 float s = static_cast<float>(static_cast<int>(raw[3][j])) * 0x1p-21f;
@@ -271,7 +296,7 @@ __global__ void __launch_bounds__(128, GemmTraits<kFmt>::kMinBlocks)
                 s = fmaf(static_cast<float>(static_cast<int>(raw[1][j])), 0x1p-7f, s);
                 s = fmaf(static_cast<float>(static_cast<int>(raw[0][j])), 1.0f, s);
                 if (diag_chunk && c0 + j == r)
-                    s = static_cast<float>(P.a_sqnorm[r] * 0x1p14);  // exact sum of squares of the represented row
+                    s = diag_exact;  // exact sum of squares of the represented row
                 out[j] = (row_scale * col_scale[chunk * 16 + j]) * (s * 0x1p-14f);
             }
         } else {
@@ -338,6 +363,7 @@ __global__ void __launch_bounds__(128, GemmTraits<kFmt>::kMinBlocks)
         }
     }
 
+    PF_GSTAMP(5, threadIdx.x == 0);
     ptx::tc_fence_before();
     __syncthreads();
     if (warp == 0) ptx::tmem_dealloc<T::kTmemCols>(tmem);
