@@ -91,8 +91,14 @@ typedef struct pf_inverse_problem {
     void* workspace; /* pf_damped_inverse_workspace(d) bytes each */
     int* d_info;
 } pf_inverse_problem;
-/* Batched: problems with equal d share every launch of the recursion. */
+/* Batched: problems with equal d advance through the recursion in lockstep;
+ * groups of different d run concurrently.  pf_set_inverse_mode selects the
+ * executor (same arithmetic, bit-identical results): 0 (default) one
+ * stream-ordered PDL launch per recursion step, groups on forked streams;
+ * 1 one persistent launch (inv_graph_kernel) walking every group's recursion
+ * as a task graph.  Returns PF_BAD_ARG for other modes. */
 int pf_damped_inverse_batched(const pf_inverse_problem* problems, int count, void* stream);
+int pf_set_inverse_mode(int mode);
 
 /* Precondition: P = B^-1 * G * A^-1 (kfac::precondition, kfac.cpp:133-137).
  * G, P: fp32 d_out x d_in row-major (ld = d_in); A^-1: d_in x d_in; B^-1:

@@ -10,6 +10,7 @@
 #include <cudaTypedefs.h>
 
 #include <algorithm>
+#include <cstdio>
 #include <cstdlib>
 #include <utility>
 #include <atomic>
@@ -20,6 +21,7 @@
 #include <vector>
 
 #include "../host/capi_common.hpp"
+#include "inv_graph.cuh"
 #include "leaf.cuh"
 #include "pf_kfac.h"
 #include "pf_sched.h"
@@ -110,6 +112,21 @@ void encode(CUtensorMap* m, const void* ptr, bool bf16, int rows, int k, size_t 
     if (r != CUDA_SUCCESS) throw CudaError("cuTensorMapEncodeTiled failed: " + std::to_string(r));
 }
 
+// 3-D map over the 4 digit planes of a sliced operand: dims {k, rows, plane},
+// box {64, 128, 4} (one TMA per operand tile per k-block).
+void encode_planes(CUtensorMap* m, const int8_t* planes, int rows, int k, int kpad, int64_t plane_stride) {
+    if (!aligned16(planes) || kpad % 16 != 0 || plane_stride % 16 != 0)
+        throw std::invalid_argument("digit planes need 16-byte aligned rows and planes");
+    const cuuint64_t dims[3] = {static_cast<cuuint64_t>(k), static_cast<cuuint64_t>(rows), 4};
+    const cuuint64_t strides[2] = {static_cast<cuuint64_t>(kpad), static_cast<cuuint64_t>(plane_stride)};
+    const cuuint32_t box[3] = {64, 128, 4};
+    const cuuint32_t estr[3] = {1, 1, 1};
+    const CUresult r = encoder()(m, CU_TENSOR_MAP_DATA_TYPE_UINT8, 3, const_cast<int8_t*>(planes), dims, strides,
+                                 box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_64B,
+                                 CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r != CUDA_SUCCESS) throw CudaError("cuTensorMapEncodeTiled(3d) failed: " + std::to_string(r));
+}
+
 // ------------------------------------------------------------ digit form
 struct Sliced {
     int8_t* planes = nullptr;
@@ -179,6 +196,51 @@ struct GemmSpec {
     int ldc = 0, ldc_t = 0;
 };
 
+// GemmSpec -> GemmDesc, encoding its operand tensor maps at maps[*n_maps...]
+// (tile_begin left to the caller).  Returns the number of maps used.
+template <int kFmt>
+int make_desc(const GemmSpec& s, GemmDesc& d, CUtensorMap* maps, int n_maps) {
+    using T = GemmTraits<kFmt>;
+    const bool shared_ab = kFmt == kBF16 ? (s.a_bf16 == s.b_bf16 && s.lda == s.ldb) : (s.a.planes == s.b.planes);
+    int m = n_maps;
+    auto put_maps = [&](bool is_a) {
+        const int first = m;
+        if constexpr (kFmt == kBF16) {
+            encode(&maps[m++], is_a ? s.a_bf16 : s.b_bf16, true, is_a ? s.rows : s.cols, s.k,
+                   static_cast<size_t>(is_a ? s.lda : s.ldb) * 2);
+        } else {
+            const Sliced& o = is_a ? s.a : s.b;
+            encode_planes(&maps[m++], o.planes, o.rows, o.k, o.kpad, o.plane_stride);
+        }
+        return first;
+    };
+    std::memset(&d, 0, sizeof(d));
+    d.a_map = put_maps(true);
+    d.b_map = shared_ab ? d.a_map : put_maps(false);
+    if (kFmt == kOZ8 && shared_ab) d.flags |= EPI_EXACT_DIAG;
+    d.rows = s.rows;
+    d.cols = s.cols;
+    d.k = s.k;
+    d.tiles_m = (s.rows + kTile - 1) / kTile;
+    d.tiles_n = (s.cols + kTile - 1) / kTile;
+    d.lower = s.lower ? 1 : 0;
+    d.k_mode = s.k_mode;
+    d.alpha = s.alpha;
+    d.beta = s.beta;
+    d.flags |= s.flags;
+    d.a_exp = s.a.exps;
+    d.b_exp = s.b.exps;
+    d.a_sqnorm = s.a.sqnorm;
+    d.c = s.c;
+    d.c_t = s.c_t;
+    d.ldc = s.ldc;
+    d.ldc_t = s.ldc_t;
+    (void)sizeof(T);
+    return m - n_maps;
+}
+
+inline int desc_tiles(const GemmDesc& d) { return d.lower ? d.tiles_m * (d.tiles_m + 1) / 2 : d.tiles_m * d.tiles_n; }
+
 template <int kFmt>
 void launch_gemms(const std::vector<GemmSpec>& specs, cudaStream_t stream) {
     using T = GemmTraits<kFmt>;
@@ -194,47 +256,11 @@ void launch_gemms(const std::vector<GemmSpec>& specs, cudaStream_t stream) {
         std::memset(&batch, 0, sizeof(batch));
         int maps = 0, probs = 0, tiles = 0;
         while (i < specs.size() && probs < kMaxProbs) {
-            const GemmSpec& s = specs[i];
-            const bool shared_ab = kFmt == kBF16 ? (s.a_bf16 == s.b_bf16 && s.lda == s.ldb)
-                                                 : (s.a.planes == s.b.planes);
-            const int need = T::kPlanes * (shared_ab ? 1 : 2);
-            if (maps + need > kMaxMaps) break;
+            if (maps + 2 > kMaxMaps) break;
             GemmDesc& d = batch.probs[probs];
-            auto put_maps = [&](bool is_a) {
-                const int first = maps;
-                if constexpr (kFmt == kBF16) {
-                    encode(&batch.maps[maps++], is_a ? s.a_bf16 : s.b_bf16, true,
-                           is_a ? s.rows : s.cols, s.k, static_cast<size_t>(is_a ? s.lda : s.ldb) * 2);
-                } else {
-                    const Sliced& o = is_a ? s.a : s.b;
-                    for (int pl = 0; pl < kDigits; ++pl)
-                        encode(&batch.maps[maps++], o.planes + pl * o.plane_stride, false, o.rows,
-                               o.k, static_cast<size_t>(o.kpad));
-                }
-                return first;
-            };
-            d.a_map = put_maps(true);
-            d.b_map = shared_ab ? d.a_map : put_maps(false);
-            if (kFmt == kOZ8 && shared_ab) d.flags |= EPI_EXACT_DIAG;
-            d.rows = s.rows;
-            d.cols = s.cols;
-            d.k = s.k;
-            d.tiles_m = (s.rows + kTile - 1) / kTile;
-            d.tiles_n = (s.cols + kTile - 1) / kTile;
-            d.lower = s.lower ? 1 : 0;
+            maps += make_desc<kFmt>(specs[i], d, batch.maps, maps);
             d.tile_begin = tiles;
-            d.k_mode = s.k_mode;
-            d.alpha = s.alpha;
-            d.beta = s.beta;
-            d.flags |= s.flags;
-            d.a_exp = s.a.exps;
-            d.b_exp = s.b.exps;
-            d.a_sqnorm = s.a.sqnorm;
-            d.c = s.c;
-            d.c_t = s.c_t;
-            d.ldc = s.ldc;
-            d.ldc_t = s.ldc_t;
-            tiles += s.lower ? d.tiles_m * (d.tiles_m + 1) / 2 : d.tiles_m * d.tiles_n;
+            tiles += desc_tiles(d);
             ++probs;
             ++i;
         }
@@ -250,13 +276,6 @@ void gemm_bf16(const std::vector<GemmSpec>& s, cudaStream_t st) { launch_gemms<k
 void gemm_oz8(const std::vector<GemmSpec>& s, cudaStream_t st) { launch_gemms<kOZ8>(s, st); }
 
 // ------------------------------------------------------------ small kernels
-struct Damp2D {
-    const float* src;
-    float* dst;
-    int* info;  // reset to 0 (success) before the factorisation
-    int d, ld_src, ld_dst;
-    float damping;
-};
 constexpr int kMaxDamp = 16;
 struct DampBatch {
     Damp2D e[kMaxDamp];
@@ -320,25 +339,115 @@ InvWs carve(void* base, int d) {
 
 float* at(float* base, int ld, int r, int c) { return base + static_cast<size_t>(r) * ld + c; }
 
-void launch_leaves(const std::vector<InvWs>& ws, int o, int n, cudaStream_t st) {
-    static std::once_flag once;
-    std::call_once(once, [] {
-        check(cudaFuncSetAttribute(leaf_chol_inv_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                   kLeafSmemBytes),
-              "cudaFuncSetAttribute(leaf)");
-    });
-    for (std::size_t i = 0; i < ws.size(); i += kMaxLeafBatch) {
-        LeafBatch b{};
-        const int cnt = static_cast<int>(std::min<std::size_t>(kMaxLeafBatch, ws.size() - i));
-        for (int j = 0; j < cnt; ++j) {
-            const InvWs& w = ws[i + j];
-            b.e[j] = LeafArgs{at(w.a, w.ld, o, o), at(w.x, w.ld, o, o), at(w.xt, w.ld, o, o),
-                              w.info, w.ld, n, o};
-        }
-        launch(leaf_chol_inv_kernel, dim3(cnt), dim3(kLeafThreads), kLeafSmemBytes, st, b);
-        after_launch("leaf_chol_inv_kernel");
-    }
+// The inversion is written once (inverse_rec) against an Emitter with two
+// back ends: StreamEmitter launches one kernel per step on a stream (the
+// reference-shaped path, kept for A/B and debugging), GraphBuilder turns each
+// step into a PHASE of tasks for the persistent inv_graph_kernel.
+struct Emitter {
+    virtual ~Emitter() = default;
+    virtual void damp(const std::vector<Damp2D>& jobs) = 0;
+    virtual void slices(const std::vector<SliceReq>& reqs) = 0;
+    virtual void gemms(const std::vector<GemmSpec>& specs) = 0;
+    virtual void leaves(const std::vector<InvWs>& ws, int o, int n) = 0;
+};
+
+LeafArgs leaf_args(const InvWs& w, int o, int n) {
+    return LeafArgs{at(w.a, w.ld, o, o), at(w.x, w.ld, o, o), at(w.xt, w.ld, o, o), w.info, w.ld, n, o};
 }
+
+SliceJob slice_job(const SliceReq& r) {
+    return SliceJob{r.src, r.dst.rows, r.dst.k, r.ld, r.mode, r.dst.planes, r.dst.plane_stride, r.dst.kpad,
+                    r.dst.exps, r.dst.sqnorm};
+}
+
+struct StreamEmitter final : Emitter {
+    cudaStream_t st;
+    explicit StreamEmitter(cudaStream_t s) : st(s) {}
+    void damp(const std::vector<Damp2D>& jobs) override {
+        DampBatch db{};
+        int d = 1;
+        for (std::size_t i = 0; i < jobs.size(); ++i) {
+            db.e[i] = jobs[i];
+            d = std::max(d, jobs[i].d);
+        }
+        const int blocks = std::min((d * d + 255) / 256, 148 * 8);
+        launch(damp_kernel, dim3(blocks, static_cast<unsigned>(jobs.size())), dim3(256), 0, st, db);
+        after_launch("damp_kernel");
+    }
+    void slices(const std::vector<SliceReq>& reqs) override { launch_slices(reqs, st); }
+    void gemms(const std::vector<GemmSpec>& specs) override { gemm_oz8(specs, st); }
+    void leaves(const std::vector<InvWs>& ws, int o, int n) override {
+        static std::once_flag once;
+        std::call_once(once, [] {
+            check(cudaFuncSetAttribute(leaf_chol_inv_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       kLeafSmemBytes),
+                  "cudaFuncSetAttribute(leaf)");
+        });
+        for (std::size_t i = 0; i < ws.size(); i += kMaxLeafBatch) {
+            LeafBatch b{};
+            const int cnt = static_cast<int>(std::min<std::size_t>(kMaxLeafBatch, ws.size() - i));
+            for (int j = 0; j < cnt; ++j) b.e[j] = leaf_args(ws[i + j], o, n);
+            launch(leaf_chol_inv_kernel, dim3(cnt), dim3(kLeafThreads), kLeafSmemBytes, st, b);
+            after_launch("leaf_chol_inv_kernel");
+        }
+    }
+};
+
+// Collects the phases of one factor group (a chain); programs interleave the
+// phase lists of independent groups.
+struct GraphBuilder final : Emitter {
+    struct Proto {
+        int type, a, b;
+    };
+    std::vector<std::vector<Proto>> phases;  // this group's chain
+    std::vector<GemmDesc>* descs;
+    std::vector<CUtensorMap>* maps;
+    std::vector<SliceJob>* slice_jobs;
+    std::vector<LeafArgs>* leaf_jobs;
+    std::vector<Damp2D>* damp_jobs;
+
+    void damp(const std::vector<Damp2D>& jobs) override {
+        std::vector<Proto> ph;
+        for (const Damp2D& j : jobs) {
+            const int idx = static_cast<int>(damp_jobs->size());
+            damp_jobs->push_back(j);
+            for (int r = 0; r < j.d; r += kGraphRows) ph.push_back({GT_DAMP, idx, r});
+        }
+        phases.push_back(std::move(ph));
+    }
+    void slices(const std::vector<SliceReq>& reqs) override {
+        std::vector<Proto> ph;
+        for (const SliceReq& r : reqs) {
+            const int idx = static_cast<int>(slice_jobs->size());
+            slice_jobs->push_back(slice_job(r));
+            for (int row = 0; row < r.dst.rows; row += kGraphRows) ph.push_back({GT_SLICE, idx, row});
+        }
+        phases.push_back(std::move(ph));
+    }
+    void gemms(const std::vector<GemmSpec>& specs) override {
+        std::vector<Proto> ph;
+        for (const GemmSpec& sp : specs) {
+            GemmDesc d;
+            const std::size_t m0 = maps->size();
+            maps->resize(m0 + 2);
+            const int used = make_desc<kOZ8>(sp, d, maps->data(), static_cast<int>(m0));
+            maps->resize(m0 + used);
+            const int idx = static_cast<int>(descs->size());
+            descs->push_back(d);
+            for (int t = 0; t < desc_tiles(d); ++t) ph.push_back({GT_GEMM, idx, t});
+        }
+        phases.push_back(std::move(ph));
+    }
+    void leaves(const std::vector<InvWs>& ws, int o, int n) override {
+        std::vector<Proto> ph;
+        for (const InvWs& w : ws) {
+            const int idx = static_cast<int>(leaf_jobs->size());
+            leaf_jobs->push_back(leaf_args(w, o, n));
+            ph.push_back({GT_LEAF, idx, 0});
+        }
+        phases.push_back(std::move(ph));
+    }
+};
 
 // Slice [rows x k] at (r0, c0) of `src` into slot `slot`.
 SliceReq slice_of(float* src, int ld, int r0, int c0, int rows, int k, void* slot, int mode) {
@@ -353,14 +462,14 @@ SliceReq slice_of(float* src, int ld, int r0, int c0, int rows, int k, void* slo
 //   recurse on A22
 //   T^T  = (L21 X11)^T          (via XT11)
 //   X21  = -X22 T,  XT12 = X21^T
-void inverse_rec(const std::vector<InvWs>& ws, int o, int n, cudaStream_t st) {
+void inverse_rec(const std::vector<InvWs>& ws, int o, int n, Emitter& em) {
     if (n <= kLeaf) {
-        launch_leaves(ws, o, n, st);
+        em.leaves(ws, o, n);
         return;
     }
     const int n1 = kTile * ((n + 2 * kTile - 1) / (2 * kTile));
     const int n2 = n - n1;
-    inverse_rec(ws, o, n1, st);
+    inverse_rec(ws, o, n1, em);
 
     std::vector<SliceReq> sl;
     std::vector<GemmSpec> g;
@@ -380,8 +489,8 @@ void inverse_rec(const std::vector<InvWs>& ws, int o, int n, cudaStream_t st) {
         s.ldc = w.ld;
         g.push_back(s);
     }
-    launch_slices(sl, st);
-    gemm_oz8(g, st);
+    em.slices(sl);
+    em.gemms(g);
     // ---- A22 -= L21 L21^T
     sl.clear();
     g.clear();
@@ -400,10 +509,10 @@ void inverse_rec(const std::vector<InvWs>& ws, int o, int n, cudaStream_t st) {
         s.ldc = w.ld;
         g.push_back(s);
     }
-    launch_slices(sl, st);
-    gemm_oz8(g, st);
+    em.slices(sl);
+    em.gemms(g);
 
-    inverse_rec(ws, o + n1, n2, st);
+    inverse_rec(ws, o + n1, n2, em);
 
     // ---- T^T = (L21 X11)^T : B operand rows = XT11 (upper block-triangular)
     sl.clear();
@@ -423,8 +532,8 @@ void inverse_rec(const std::vector<InvWs>& ws, int o, int n, cudaStream_t st) {
         s.ldc = w.ld;
         g.push_back(s);
     }
-    launch_slices(sl, st);
-    gemm_oz8(g, st);
+    em.slices(sl);
+    em.gemms(g);
     // ---- X21 = -X22 T  (B operand rows = T^T), also stored as XT12
     sl.clear();
     g.clear();
@@ -446,25 +555,22 @@ void inverse_rec(const std::vector<InvWs>& ws, int o, int n, cudaStream_t st) {
         s.ldc_t = w.ld;
         g.push_back(s);
     }
-    launch_slices(sl, st);
-    gemm_oz8(g, st);
+    em.slices(sl);
+    em.gemms(g);
 }
 
-void damped_inverse_group(const std::vector<const pf_inverse_problem*>& probs, cudaStream_t st) {
+void damped_inverse_group(const std::vector<const pf_inverse_problem*>& probs, Emitter& em) {
     const int d = probs.front()->d;
     std::vector<InvWs> ws;
-    DampBatch db{};
-    for (std::size_t i = 0; i < probs.size(); ++i) {
-        const pf_inverse_problem* p = probs[i];
+    std::vector<Damp2D> damps;
+    for (const pf_inverse_problem* p : probs) {
         InvWs w = carve(p->workspace, d);
         w.info = p->d_info;
-        db.e[i] = Damp2D{p->m, w.a, p->d_info, d, p->ldm, w.ld, p->damping};
+        damps.push_back(Damp2D{p->m, w.a, p->d_info, d, p->ldm, w.ld, p->damping});
         ws.push_back(w);
     }
-    const int blocks = std::min((d * d + 255) / 256, 148 * 8);
-    launch(damp_kernel, dim3(blocks, static_cast<unsigned>(probs.size())), dim3(256), 0, st, db);
-    after_launch("damp_kernel");
-    inverse_rec(ws, 0, d, st);
+    em.damp(damps);
+    inverse_rec(ws, 0, d, em);
     // ---- LAUUM: M^-1 = X^T X = XT XT^T  (lower tiles, mirrored)
     std::vector<SliceReq> sl;
     std::vector<GemmSpec> g;
@@ -484,14 +590,167 @@ void damped_inverse_group(const std::vector<const pf_inverse_problem*>& probs, c
         s.ldc = p->ldinv;
         g.push_back(s);
     }
-    launch_slices(sl, st);
-    gemm_oz8(g, st);
+    em.slices(sl);
+    em.gemms(g);
     sl.clear();
     for (const pf_inverse_problem* p : probs)
         if (p->minv_sliced)
             sl.push_back(SliceReq{p->minv, p->ldinv, SLICE_FULL, sliced_view(p->minv_sliced, d, d)});
-    launch_slices(sl, st);
+    if (!sl.empty()) em.slices(sl);
 }
+
+// ------------------------------------------------------------ task-graph programs
+// A device-resident program for inv_graph_kernel, built once per distinct
+// problem list (pointers, sizes, damping) and cached: steady-state calls (and
+// CUDA-graph replays) only reset the counters and launch.  Entries are never
+// freed (captured graphs may reference them).
+struct GraphProg {
+    GraphProgram prog{};
+    int n_phases = 0;
+    int* counters = nullptr;  // phase_done[n_phases] + cursor
+    int grid = 0;
+};
+
+std::mutex g_prog_mu;
+std::vector<std::pair<std::string, GraphProg*>> g_progs;
+
+template <class V>
+std::size_t put_bytes(std::vector<uint8_t>& buf, const V& v, std::size_t align) {
+    const std::size_t off = (buf.size() + align - 1) / align * align;
+    buf.resize(off + v.size() * sizeof(typename V::value_type));
+    if (!v.empty()) std::memcpy(buf.data() + off, v.data(), v.size() * sizeof(typename V::value_type));
+    return off;
+}
+
+GraphProg* build_program(const std::vector<std::vector<const pf_inverse_problem*>>& groups, cudaStream_t st) {
+    std::vector<GemmDesc> gemms;
+    std::vector<CUtensorMap> maps;
+    std::vector<SliceJob> slice_jobs;
+    std::vector<LeafArgs> leaf_jobs;
+    std::vector<Damp2D> damp_jobs;
+    std::vector<GraphBuilder> chains(groups.size());
+    for (std::size_t gi = 0; gi < groups.size(); ++gi) {
+        GraphBuilder& b = chains[gi];
+        b.descs = &gemms;
+        b.maps = &maps;
+        b.slice_jobs = &slice_jobs;
+        b.leaf_jobs = &leaf_jobs;
+        b.damp_jobs = &damp_jobs;
+        damped_inverse_group(groups[gi], b);
+    }
+    // interleave the chains phase by phase: round r holds phase r of every
+    // group, so a task only ever waits on lower-indexed tasks
+    std::vector<GraphTask> tasks;
+    std::vector<int> phase_size;
+    std::vector<int> last(groups.size(), -1);
+    std::size_t rounds = 0;
+    for (const GraphBuilder& b : chains) rounds = std::max(rounds, b.phases.size());
+    for (std::size_t r = 0; r < rounds; ++r)
+        for (std::size_t gi = 0; gi < chains.size(); ++gi) {
+            if (r >= chains[gi].phases.size() || chains[gi].phases[r].empty()) continue;
+            const int ph = static_cast<int>(phase_size.size());
+            phase_size.push_back(static_cast<int>(chains[gi].phases[r].size()));
+            for (const GraphBuilder::Proto& pr : chains[gi].phases[r])
+                tasks.push_back(GraphTask{pr.type, ph, last[gi], pr.a, pr.b});
+            last[gi] = ph;
+        }
+    std::vector<uint8_t> buf;
+    const std::size_t o_tasks = put_bytes(buf, tasks, 16);
+    const std::size_t o_size = put_bytes(buf, phase_size, 16);
+    const std::size_t o_gemm = put_bytes(buf, gemms, 16);
+    const std::size_t o_maps = put_bytes(buf, maps, 128);
+    const std::size_t o_slice = put_bytes(buf, slice_jobs, 16);
+    const std::size_t o_leaf = put_bytes(buf, leaf_jobs, 16);
+    const std::size_t o_damp = put_bytes(buf, damp_jobs, 16);
+    auto* gp = new GraphProg;
+    uint8_t* dev = nullptr;
+    void* host = nullptr;
+    check(cudaMalloc(&dev, buf.size() + 256), "cudaMalloc(program)");
+    check(cudaMalloc(&gp->counters, (phase_size.size() + 1) * sizeof(int)), "cudaMalloc(counters)");
+    check(cudaMallocHost(&host, buf.size()), "cudaMallocHost(program)");
+    std::memcpy(host, buf.data(), buf.size());
+    check(cudaMemcpyAsync(dev, host, buf.size(), cudaMemcpyHostToDevice, st), "upload program");
+    gp->n_phases = static_cast<int>(phase_size.size());
+    GraphProgram& P = gp->prog;
+    P.tasks = reinterpret_cast<const GraphTask*>(dev + o_tasks);
+    P.n_tasks = static_cast<int>(tasks.size());
+    P.phase_size = reinterpret_cast<const int*>(dev + o_size);
+    P.phase_done = gp->counters;
+    P.cursor = gp->counters + gp->n_phases;
+    P.gemms = reinterpret_cast<const GemmDesc*>(dev + o_gemm);
+    P.maps = reinterpret_cast<const CUtensorMap*>(dev + o_maps);
+    P.slices = reinterpret_cast<const SliceJob*>(dev + o_slice);
+    P.leaves = reinterpret_cast<const LeafArgs*>(dev + o_leaf);
+    P.damps = reinterpret_cast<const Damp2D*>(dev + o_damp);
+    int dev_id = 0, sms = 148;
+    check(cudaGetDevice(&dev_id), "cudaGetDevice");
+    check(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev_id), "SM count");
+    gp->grid = std::max(1, std::min(sms, P.n_tasks));
+    return gp;
+}
+
+std::string program_key(const std::vector<std::vector<const pf_inverse_problem*>>& groups) {
+    std::string k;
+    int dev = 0;
+    cudaGetDevice(&dev);
+    k.append(reinterpret_cast<const char*>(&dev), sizeof(dev));
+    for (const auto& g : groups) {
+        const char sep = '|';
+        k.push_back(sep);
+        for (const pf_inverse_problem* p : g) k.append(reinterpret_cast<const char*>(p), sizeof(*p));
+    }
+    return k;
+}
+
+void run_program(const std::vector<std::vector<const pf_inverse_problem*>>& groups, cudaStream_t st) {
+    GraphProg* gp = nullptr;
+    {
+        const std::string key = program_key(groups);
+        std::lock_guard<std::mutex> lk(g_prog_mu);
+        for (auto& kv : g_progs)
+            if (kv.first == key) gp = kv.second;
+        if (!gp) {
+            gp = build_program(groups, st);
+            g_progs.emplace_back(key, gp);
+        }
+    }
+    static std::once_flag once;
+    std::call_once(once, [] {
+        check(cudaFuncSetAttribute(inv_graph_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kGraphSmemBytes),
+              "cudaFuncSetAttribute(inv_graph)");
+    });
+    check(cudaMemsetAsync(gp->counters, 0, (gp->n_phases + 1) * sizeof(int), st), "reset counters");
+    // PF_INV_TRACE=<file>: development timeline (eager calls only; synchronises)
+    static const char* trace_path = std::getenv("PF_INV_TRACE");
+    GraphProgram prog = gp->prog;
+    unsigned long long* trace = nullptr;
+    if (trace_path) {
+        check(cudaMalloc(&trace, sizeof(unsigned long long) * 8 * prog.n_tasks), "cudaMalloc(trace)");
+        check(cudaMemsetAsync(trace, 0, sizeof(unsigned long long) * 8 * prog.n_tasks, st), "trace reset");
+        prog.trace = trace;
+    }
+    launch(inv_graph_kernel, dim3(gp->grid), dim3(kGraphThreads), kGraphSmemBytes, st, prog);
+    after_launch("inv_graph_kernel");
+    if (trace) {
+        std::vector<unsigned long long> h(8 * static_cast<std::size_t>(prog.n_tasks));
+        std::vector<GraphTask> tasks(prog.n_tasks);
+        check(cudaStreamSynchronize(st), "trace sync");
+        check(cudaMemcpy(h.data(), trace, h.size() * 8, cudaMemcpyDeviceToHost), "trace copy");
+        check(cudaMemcpy(tasks.data(), prog.tasks, tasks.size() * sizeof(GraphTask), cudaMemcpyDeviceToHost),
+              "trace tasks");
+        if (FILE* f = std::fopen(trace_path, "w")) {
+            std::fprintf(f, "task,type,phase,wait,a,b,claimed_ns,ready_ns,done_ns,sm,mma_issued,pre_wait,acc_ready,epi_end\n");
+            for (int t = 0; t < prog.n_tasks; ++t)
+                std::fprintf(f, "%d,%d,%d,%d,%d,%d,%llu,%llu,%llu,%llu,%llu,%llu,%llu,%llu\n", t, tasks[t].type,
+                             tasks[t].phase, tasks[t].wait, tasks[t].a, tasks[t].b, h[8 * t], h[8 * t + 1],
+                             h[8 * t + 2], h[8 * t + 3], h[8 * t + 4], h[8 * t + 5], h[8 * t + 6], h[8 * t + 7]);
+            std::fclose(f);
+        }
+        cudaFree(trace);
+    }
+}
+
+std::atomic<int> g_inverse_mode{0};  // 0 one launch per step (default), 1 persistent task graph
 
 // ------------------------------------------------------------ precondition
 // workspace: digit forms of A^-1, B^-1 (when given as fp32), G, U^T; fp32 U^T
@@ -711,6 +970,12 @@ int pf_slice(const float* x, int rows, int k, int ld, void* sliced, void* stream
     });
 }
 
+int pf_set_inverse_mode(int mode) {
+    if (mode != 0 && mode != 1) return PF_BAD_ARG;
+    g_inverse_mode.store(mode);
+    return 0;
+}
+
 int pf_damped_inverse_workspace(int d, size_t* bytes) {
     return pf_detail::guard([&] {
         if (d < 1 || !bytes) throw std::invalid_argument("bad d");
@@ -748,7 +1013,14 @@ int pf_damped_inverse_batched(const pf_inverse_problem* problems, int count, voi
             i = j;
         }
         const cudaStream_t st = static_cast<cudaStream_t>(stream);
-        run_forked(groups.size(), st, [&](std::size_t g, cudaStream_t s) { damped_inverse_group(groups[g], s); });
+        if (g_inverse_mode.load() == 1) {
+            run_program(groups, st);  // one persistent launch for every group
+        } else {
+            run_forked(groups.size(), st, [&](std::size_t g, cudaStream_t s) {
+                StreamEmitter em(s);
+                damped_inverse_group(groups[g], em);
+            });
+        }
         return 0;
     });
 }

@@ -281,7 +281,7 @@ __device__ __forceinline__ void load_lower(float* dst, const float* src, int ld,
         for (int q = 0; q < kPer; ++q) {
             const int idx = tid + q * kLeafThreads;
             const int r = idx / (kLeaf / 4), c = 4 * (idx % (kLeaf / 4));
-            v[q] = (c <= r) ? *reinterpret_cast<const float4*>(src + (size_t)r * ld + c)
+            v[q] = (c <= r) ? __ldcg(reinterpret_cast<const float4*>(src + (size_t)r * ld + c))
                             : make_float4(0.f, 0.f, 0.f, 0.f);
         }
 #pragma unroll
@@ -299,7 +299,7 @@ __device__ __forceinline__ void load_lower(float* dst, const float* src, int ld,
             const int r = idx / kLeaf, c = idx % kLeaf;
             float v;
             if (r < n && c < n)
-                v = (c <= r) ? src[(size_t)r * ld + c] : 0.0f;
+                v = (c <= r) ? __ldcg(src + (size_t)r * ld + c) : 0.0f;
             else
                 v = (r == c) ? 1.0f : 0.0f;
             dst[r * kLeafPitch + c] = v;
@@ -353,8 +353,9 @@ __device__ __forceinline__ void report_bad(int* info, int bad) {
     }
 }
 
-__global__ void __launch_bounds__(kLeafThreads, 1) leaf_chol_inv_kernel(const __grid_constant__ LeafBatch batch) {
-    extern __shared__ __align__(16) float leaf_smem[];
+// The whole leaf for one block, 256 threads, `leaf_smem` = kLeafSmemBytes of
+// 16-byte aligned shared memory.  `pdl`: called from a PDL-launched kernel.
+__device__ __forceinline__ void leaf_body(const LeafArgs& A, float* leaf_smem, bool pdl) {
     float* Ls = leaf_smem;
     float* Xs = Ls + kLsFloats;
     float* PT = Xs + kXsFloats;  // panels 0..2, transposed
@@ -364,7 +365,6 @@ __global__ void __launch_bounds__(kLeafThreads, 1) leaf_chol_inv_kernel(const __
     float* lbuf = Tb + kTbFloats;  // chol32 broadcast buffer, 2 x 32
     float* rdiag = lbuf + 64;
     int* bad = reinterpret_cast<int*>(rdiag + kLeaf);
-    const LeafArgs& A = batch.e[blockIdx.x];
     const int tid = threadIdx.x;
     const int warp = tid >> 5;
 
@@ -372,7 +372,7 @@ __global__ void __launch_bounds__(kLeafThreads, 1) leaf_chol_inv_kernel(const __
     if (tid == 0) *bad = INT_MAX;
     zero_upper_blocks(Xs);
     PF_STAMP(1);
-    ptx::grid_dep_wait();  // PDL: A is produced by the previous launch
+    if (pdl) ptx::grid_dep_wait();  // PDL: A is produced by the previous launch
     load_lower(Ls, A.a, A.ld, A.n);
     __syncthreads();
     PF_STAMP(2);
@@ -430,10 +430,15 @@ __global__ void __launch_bounds__(kLeafThreads, 1) leaf_chol_inv_kernel(const __
     for (int t = tid; t < 192; t += kLeafThreads) xprod_tile(XTd, Tb, Xs, 3, t / 24, t % 24);
     __syncthreads();
     PF_STAMP(14);
-    ptx::grid_dep_launch();
+    if (pdl) ptx::grid_dep_launch();
     store_x(Xs, A.x, A.xt, A.ld, A.n);
     PF_STAMP(19);
     if (tid == 0) report_bad(A.info, *bad);
+}
+
+__global__ void __launch_bounds__(kLeafThreads, 1) leaf_chol_inv_kernel(const __grid_constant__ LeafBatch batch) {
+    extern __shared__ __align__(16) float leaf_smem[];
+    leaf_body(batch.e[blockIdx.x], leaf_smem, true);
 }
 
 }  // namespace pf

@@ -69,16 +69,11 @@ __device__ __forceinline__ void slice_digits(float x, int e, int8_t (&q)[4], dou
           static_cast<double>(q2) * 0x1p-21 + static_cast<double>(q3) * 0x1p-28;
 }
 
-// one warp per row; grid (ceil(rows / 8), jobs).  Rows whose valid range is
-// 16-byte aligned move 4 elements per lane per access (float4 in, char4 out)
-// with 4 accesses in flight per lane.
-__global__ void __launch_bounds__(256) slice_kernel(const __grid_constant__ SliceBatch b) {
-    const SliceJob& J = b.j[blockIdx.y];
-    const int r = blockIdx.x * 8 + (threadIdx.x >> 5);
-    const int lane = threadIdx.x & 31;
-    ptx::grid_dep_wait();  // PDL: the rows are produced by the previous launch
-    ptx::grid_dep_launch();
-    if (r >= J.rows) return;
+// One warp slices row r of job J.  Rows whose valid range is 16-byte aligned
+// move 4 elements per lane per access (float4 in, char4 out) with 4 accesses
+// in flight per lane.  Loads bypass L1 (ld.global.cg): in the persistent
+// inversion kernel the rows were written by other SMs moments earlier.
+__device__ __forceinline__ void slice_row(const SliceJob& J, int r, int lane) {
     int lo, hi;
     valid_range(J, r, lo, hi);
     const float* row = J.src + static_cast<int64_t>(r) * J.ld;
@@ -86,6 +81,48 @@ __global__ void __launch_bounds__(256) slice_kernel(const __grid_constant__ Slic
     const bool vec = ((reinterpret_cast<uintptr_t>(row + lo) & 15) == 0) && ((hi - lo) % 4 == 0) &&
                      ((reinterpret_cast<uintptr_t>(p0 + lo) & 3) == 0) && (J.plane_stride % 4 == 0);
     float m = 0.0f;
+    if (vec && hi - lo <= 1024) {
+        // short row (every inversion operand up to d = 1024): ONE pass over
+        // global memory, the row stays in registers between max and digits
+        const float4* r4 = reinterpret_cast<const float4*>(row + lo);
+        const int n4 = (hi - lo) / 4;
+        float4 v[8];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) v[u] = (lane + 32 * u < n4) ? __ldcg(r4 + lane + 32 * u) : make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll
+        for (int u = 0; u < 8; ++u)
+            m = fmaxf(m, fmaxf(fmaxf(fabsf(v[u].x), fabsf(v[u].y)), fmaxf(fabsf(v[u].z), fabsf(v[u].w))));
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, o));
+        int e = 0;
+        if (m > 0.0f) frexpf(m, &e);
+        if (lane == 0) J.exps[r] = e;
+        double sq = 0.0;
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+            const int c = lane + 32 * u;
+            if (c >= n4) continue;
+            const float xs[4] = {v[u].x, v[u].y, v[u].z, v[u].w};
+            uint32_t packed[4] = {0u, 0u, 0u, 0u};
+#pragma unroll
+            for (int w = 0; w < 4; ++w) {
+                int8_t q[4];
+                double rep;
+                slice_digits(xs[w], e, q, rep);
+                sq = fma(rep, rep, sq);
+#pragma unroll
+                for (int pl = 0; pl < 4; ++pl)
+                    packed[pl] |= static_cast<uint32_t>(static_cast<uint8_t>(q[pl])) << (8 * w);
+            }
+#pragma unroll
+            for (int pl = 0; pl < 4; ++pl)
+                *reinterpret_cast<uint32_t*>(p0 + lo + 4 * c + pl * J.plane_stride) = packed[pl];
+        }
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) sq += __shfl_xor_sync(0xffffffffu, sq, o);
+        if (lane == 0) J.sqnorm[r] = sq;
+        return;
+    }
     if (vec) {
         const float4* r4 = reinterpret_cast<const float4*>(row + lo);
         const int n4 = (hi - lo) / 4;
@@ -93,17 +130,17 @@ __global__ void __launch_bounds__(256) slice_kernel(const __grid_constant__ Slic
         for (; c + 96 < n4; c += 128) {
             float4 v[4];
 #pragma unroll
-            for (int u = 0; u < 4; ++u) v[u] = r4[c + 32 * u];
+            for (int u = 0; u < 4; ++u) v[u] = __ldcg(r4 + c + 32 * u);
 #pragma unroll
             for (int u = 0; u < 4; ++u)
                 m = fmaxf(m, fmaxf(fmaxf(fabsf(v[u].x), fabsf(v[u].y)), fmaxf(fabsf(v[u].z), fabsf(v[u].w))));
         }
         for (; c < n4; c += 32) {
-            const float4 v = r4[c];
+            const float4 v = __ldcg(r4 + c);
             m = fmaxf(m, fmaxf(fmaxf(fabsf(v.x), fabsf(v.y)), fmaxf(fabsf(v.z), fabsf(v.w))));
         }
     } else {
-        for (int c = lo + lane; c < hi; c += 32) m = fmaxf(m, fabsf(row[c]));
+        for (int c = lo + lane; c < hi; c += 32) m = fmaxf(m, fabsf(__ldcg(row + c)));
     }
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, o));
@@ -119,7 +156,7 @@ __global__ void __launch_bounds__(256) slice_kernel(const __grid_constant__ Slic
         const float4* r4 = reinterpret_cast<const float4*>(row + lo);
         const int n4 = (hi - lo) / 4;
         for (int c = lane; c < n4; c += 32) {
-            const float4 v = r4[c];
+            const float4 v = __ldcg(r4 + c);
             const float xs[4] = {v.x, v.y, v.z, v.w};
             uint32_t packed[4] = {0u, 0u, 0u, 0u};
 #pragma unroll
@@ -140,7 +177,7 @@ __global__ void __launch_bounds__(256) slice_kernel(const __grid_constant__ Slic
         for (int c = lo + lane; c < hi; c += 32) {
             int8_t q[4];
             double rep;
-            slice_digits(row[c], e, q, rep);
+            slice_digits(__ldcg(row + c), e, q, rep);
             sq = fma(rep, rep, sq);
 #pragma unroll
             for (int pl = 0; pl < 4; ++pl) p0[c + pl * J.plane_stride] = q[pl];
@@ -149,6 +186,16 @@ __global__ void __launch_bounds__(256) slice_kernel(const __grid_constant__ Slic
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) sq += __shfl_xor_sync(0xffffffffu, sq, o);
     if (lane == 0) J.sqnorm[r] = sq;
+}
+
+// one warp per row; grid (ceil(rows / 8), jobs)
+__global__ void __launch_bounds__(256) slice_kernel(const __grid_constant__ SliceBatch b) {
+    const SliceJob& J = b.j[blockIdx.y];
+    const int r = blockIdx.x * 8 + (threadIdx.x >> 5);
+    ptx::grid_dep_wait();  // PDL: the rows are produced by the previous launch
+    ptx::grid_dep_launch();
+    if (r >= J.rows) return;
+    slice_row(J, r, threadIdx.x & 31);
 }
 
 }  // namespace pf

@@ -70,7 +70,7 @@ enum KMode : int {
 };
 
 struct GemmDesc {
-    int a_map, b_map;   // index of the first plane's CUtensorMap (digit s = +s)
+    int a_map, b_map;   // CUtensorMap index per operand (kOZ8: 3-D map over the 4 digit planes)
     int rows, cols, k;
     int tiles_m, tiles_n;
     int lower;          // enumerate only tiles with tm >= tn
@@ -116,6 +116,123 @@ __device__ __forceinline__ void decode_lower(int t, int& tm, int& tn) {
     while (m * (m + 1) / 2 > t) --m;
     tm = m;
     tn = t - m * (m + 1) / 2;
+}
+
+// Epilogue of one 128x128 tile for the calling thread's TMEM lane (= tile row
+// r), chunks [chunk_begin, chunk_end) of 16 columns: TMEM -> registers ->
+// (alpha, digit recombination, beta) -> global.  Shared by the standalone
+// kernel (4 warps x 8 chunks) and the persistent inversion kernel (8 warps x
+// 4 chunks).  Global reads use ld.global.cg (data may come from other SMs of
+// the same persistent launch).
+template <int kFmt>
+__device__ __forceinline__ void epilogue_chunks(const GemmDesc& P, int tm, int tn, uint32_t lane_base, int r,
+                                                const float* col_scale, int chunk_begin, int chunk_end,
+                                                bool have_acc) {
+    const bool row_ok = r < P.rows;
+    const uint32_t f = P.flags;
+    const bool mirror = (f & EPI_MIRROR) && tm != tn;
+    float row_scale = 1.0f;
+    const bool exact_diag = (f & EPI_EXACT_DIAG) && tm == tn && row_ok;
+    float diag_exact = 0.0f;
+    if constexpr (kFmt == kOZ8) {
+        if (row_ok) row_scale = P.alpha * ptx::pow2f(__ldcg(P.a_exp + r));
+        if (exact_diag) diag_exact = static_cast<float>(__ldcg(P.a_sqnorm + r) * 0x1p14);
+    }
+#pragma unroll 1
+    for (int chunk = chunk_begin; chunk < chunk_end; ++chunk) {
+        __syncwarp();  // tcgen05.ld is .sync.aligned: re-converge first
+        const int c0 = tn * kTile + chunk * 16;
+        float out[16];
+        if constexpr (kFmt == kOZ8) {
+            // accumulator g counts units of 2^-7(g+2) of 2^(e_a + e_b); the four
+            // exact int32 sums are recombined smallest-first in fp32 (the result
+            // is stored in fp32: ~1 ulp, no accumulation error)
+            uint32_t raw[kDigits][16];
+            if (have_acc) {
+#pragma unroll
+                for (int g = 0; g < kDigits; ++g) ptx::tmem_ld16_nowait(lane_base + g * 128 + chunk * 16, raw[g]);
+                ptx::tmem_wait_ld();
+            } else {
+#pragma unroll
+                for (int g = 0; g < kDigits; ++g)
+#pragma unroll
+                    for (int j = 0; j < 16; ++j) raw[g][j] = 0u;
+            }
+            const bool diag_chunk = exact_diag && r >= c0 && r < c0 + 16;
+#pragma unroll
+            for (int j = 0; j < 16; ++j) {
+                float s = static_cast<float>(static_cast<int>(raw[3][j])) * 0x1p-21f;
+                s = fmaf(static_cast<float>(static_cast<int>(raw[2][j])), 0x1p-14f, s);
+                s = fmaf(static_cast<float>(static_cast<int>(raw[1][j])), 0x1p-7f, s);
+                s = fmaf(static_cast<float>(static_cast<int>(raw[0][j])), 1.0f, s);
+                if (diag_chunk && c0 + j == r)
+                    s = diag_exact;  // exact sum of squares of the represented row
+                out[j] = (row_scale * col_scale[chunk * 16 + j]) * (s * 0x1p-14f);
+            }
+        } else {
+            float v[16];
+            if (have_acc) {
+                ptx::tmem_ld16(lane_base + chunk * 16, v);
+            } else {
+#pragma unroll
+                for (int j = 0; j < 16; ++j) v[j] = 0.0f;
+            }
+#pragma unroll
+            for (int j = 0; j < 16; ++j) out[j] = P.alpha * v[j];
+        }
+        if (!row_ok || c0 >= P.cols) continue;
+        const bool full_chunk = c0 + 16 <= P.cols;
+        if (P.beta != 0.0f) {
+            float cv[16];
+            if ((f & EPI_VEC4) && full_chunk && !(f & EPI_TRANSPOSE)) {
+                const float4* src = reinterpret_cast<const float4*>(P.c + static_cast<size_t>(r) * P.ldc + c0);  // read via ld.cg below
+#pragma unroll
+                for (int q = 0; q < 4; ++q) {
+                    const float4 t = __ldcg(src + q);
+                    cv[4 * q] = t.x;
+                    cv[4 * q + 1] = t.y;
+                    cv[4 * q + 2] = t.z;
+                    cv[4 * q + 3] = t.w;
+                }
+            } else {
+#pragma unroll
+                for (int j = 0; j < 16; ++j) {
+                    const int c = c0 + j;
+                    const size_t idx = (f & EPI_TRANSPOSE) ? static_cast<size_t>(c) * P.ldc + r
+                                                           : static_cast<size_t>(r) * P.ldc + c;
+                    cv[j] = c < P.cols ? __ldcg(P.c + idx) : 0.0f;
+                }
+            }
+#pragma unroll
+            for (int j = 0; j < 16; ++j) out[j] = fmaf(P.beta, cv[j], out[j]);
+        }
+        if ((f & EPI_VEC4) && full_chunk && !(f & EPI_TRANSPOSE)) {
+            float4* dst = reinterpret_cast<float4*>(P.c + static_cast<size_t>(r) * P.ldc + c0);
+#pragma unroll
+            for (int q = 0; q < 4; ++q)
+                dst[q] = make_float4(out[4 * q], out[4 * q + 1], out[4 * q + 2], out[4 * q + 3]);
+        } else if (f & EPI_TRANSPOSE) {
+            // lanes hold consecutive rows -> each transposed column store is coalesced
+#pragma unroll
+            for (int j = 0; j < 16; ++j)
+                if (c0 + j < P.cols) P.c[static_cast<size_t>(c0 + j) * P.ldc + r] = out[j];
+        } else {
+#pragma unroll
+            for (int j = 0; j < 16; ++j)
+                if (c0 + j < P.cols) P.c[static_cast<size_t>(r) * P.ldc + c0 + j] = out[j];
+        }
+        if (mirror) {
+#pragma unroll
+            for (int j = 0; j < 16; ++j)
+                if (c0 + j < P.cols) P.c[static_cast<size_t>(c0 + j) * P.ldc + r] = out[j];
+        }
+        if (f & EPI_ALSO_T) {
+#pragma unroll
+            for (int j = 0; j < 16; ++j)
+                if (c0 + j < P.cols) P.c_t[static_cast<size_t>(c0 + j) * P.ldc_t + r] = out[j];
+        }
+    }
+
 }
 
 template <int kFmt>
@@ -166,11 +283,9 @@ __global__ void __launch_bounds__(128, GemmTraits<kFmt>::kMinBlocks)
         ptx::fence_barrier_init();
     }
     if (warp == 0) ptx::tmem_alloc<T::kTmemCols>(tmem_slot);
-    if (warp == 0 && lane == 0) {
-        for (int pl = 0; pl < T::kPlanes; ++pl) {
-            ptx::prefetch_tmap(&batch.maps[P.a_map + pl]);
-            ptx::prefetch_tmap(&batch.maps[P.b_map + pl]);
-        }
+    if (warp == 0 && lane == 0) {  // one map per operand (kOZ8: 3-D, all digit planes)
+        ptx::prefetch_tmap(&batch.maps[P.a_map]);
+        ptx::prefetch_tmap(&batch.maps[P.b_map]);
     }
     ptx::grid_dep_wait();  // operands, scales and C come from earlier launches
     if constexpr (kFmt == kOZ8) {
@@ -196,9 +311,12 @@ __global__ void __launch_bounds__(128, GemmTraits<kFmt>::kMinBlocks)
             ptx::mbar_wait(&empty[s], ph ^ 1u);
             ptx::mbar_arrive_expect_tx(&full[s], T::kStageBytes);
             const int kc = kb * T::kKBlock;
-            for (int pl = 0; pl < T::kPlanes; ++pl) {
-                ptx::tma_load_2d(a_plane(s, pl), &batch.maps[P.a_map + pl], &full[s], kc, tm * kTile);
-                ptx::tma_load_2d(b_plane(s, pl), &batch.maps[P.b_map + pl], &full[s], kc, tn * kTile);
+            if constexpr (kFmt == kOZ8) {
+                ptx::tma_load_3d(a_plane(s, 0), &batch.maps[P.a_map], &full[s], kc, tm * kTile, 0);
+                ptx::tma_load_3d(b_plane(s, 0), &batch.maps[P.b_map], &full[s], kc, tn * kTile, 0);
+            } else {
+                ptx::tma_load_2d(a_plane(s, 0), &batch.maps[P.a_map], &full[s], kc, tm * kTile);
+                ptx::tma_load_2d(b_plane(s, 0), &batch.maps[P.b_map], &full[s], kc, tn * kTile);
             }
             if (++s == kStages) {
                 s = 0;
@@ -256,112 +374,8 @@ __global__ void __launch_bounds__(128, GemmTraits<kFmt>::kMinBlocks)
     PF_GSTAMP(4, threadIdx.x == 0);
     ptx::grid_dep_launch();  // main loop done: let the next launch start its prologue
     __syncwarp();
-    const int r = tm * kTile + warp * 32 + static_cast<int>(lane);
-    const bool row_ok = r < P.rows;
-    const uint32_t f = P.flags;
-    const bool mirror = (f & EPI_MIRROR) && tm != tn;
-    const uint32_t lane_base = tmem + (static_cast<uint32_t>(warp * 32) << 16);
-    float row_scale = 1.0f;
-    const bool exact_diag = (f & EPI_EXACT_DIAG) && tm == tn && row_ok;
-    float diag_exact = 0.0f;
-    if constexpr (kFmt == kOZ8) {
-        if (row_ok) row_scale = P.alpha * ptx::pow2f(P.a_exp[r]);
-        if (exact_diag) diag_exact = static_cast<float>(P.a_sqnorm[r] * 0x1p14);
-    }
-#pragma unroll 1
-    for (int chunk = 0; chunk < kTile / 16; ++chunk) {
-        __syncwarp();  // tcgen05.ld is .sync.aligned: re-converge first
-        const int c0 = tn * kTile + chunk * 16;
-        float out[16];
-        if constexpr (kFmt == kOZ8) {
-            // accumulator g counts units of 2^-7(g+2) of 2^(e_a + e_b); the four
-            // exact int32 sums are recombined smallest-first in fp32 (the result
-            // is stored in fp32: ~1 ulp, no accumulation error)
-            uint32_t raw[kDigits][16];
-            if (have_acc) {
-#pragma unroll
-                for (int g = 0; g < kDigits; ++g) ptx::tmem_ld16_nowait(lane_base + g * 128 + chunk * 16, raw[g]);
-                ptx::tmem_wait_ld();
-            } else {
-#pragma unroll
-                for (int g = 0; g < kDigits; ++g)
-#pragma unroll
-                    for (int j = 0; j < 16; ++j) raw[g][j] = 0u;
-            }
-            const bool diag_chunk = exact_diag && r >= c0 && r < c0 + 16;
-#pragma unroll
-            for (int j = 0; j < 16; ++j) {
-                float s = static_cast<float>(static_cast<int>(raw[3][j])) * 0x1p-21f;
-                s = fmaf(static_cast<float>(static_cast<int>(raw[2][j])), 0x1p-14f, s);
-                s = fmaf(static_cast<float>(static_cast<int>(raw[1][j])), 0x1p-7f, s);
-                s = fmaf(static_cast<float>(static_cast<int>(raw[0][j])), 1.0f, s);
-                if (diag_chunk && c0 + j == r)
-                    s = diag_exact;  // exact sum of squares of the represented row
-                out[j] = (row_scale * col_scale[chunk * 16 + j]) * (s * 0x1p-14f);
-            }
-        } else {
-            float v[16];
-            if (have_acc) {
-                ptx::tmem_ld16(lane_base + chunk * 16, v);
-            } else {
-#pragma unroll
-                for (int j = 0; j < 16; ++j) v[j] = 0.0f;
-            }
-#pragma unroll
-            for (int j = 0; j < 16; ++j) out[j] = P.alpha * v[j];
-        }
-        if (!row_ok || c0 >= P.cols) continue;
-        const bool full_chunk = c0 + 16 <= P.cols;
-        if (P.beta != 0.0f) {
-            float cv[16];
-            if ((f & EPI_VEC4) && full_chunk && !(f & EPI_TRANSPOSE)) {
-                const float4* src = reinterpret_cast<const float4*>(P.c + static_cast<size_t>(r) * P.ldc + c0);
-#pragma unroll
-                for (int q = 0; q < 4; ++q) {
-                    const float4 t = src[q];
-                    cv[4 * q] = t.x;
-                    cv[4 * q + 1] = t.y;
-                    cv[4 * q + 2] = t.z;
-                    cv[4 * q + 3] = t.w;
-                }
-            } else {
-#pragma unroll
-                for (int j = 0; j < 16; ++j) {
-                    const int c = c0 + j;
-                    const size_t idx = (f & EPI_TRANSPOSE) ? static_cast<size_t>(c) * P.ldc + r
-                                                           : static_cast<size_t>(r) * P.ldc + c;
-                    cv[j] = c < P.cols ? P.c[idx] : 0.0f;
-                }
-            }
-#pragma unroll
-            for (int j = 0; j < 16; ++j) out[j] = fmaf(P.beta, cv[j], out[j]);
-        }
-        if ((f & EPI_VEC4) && full_chunk && !(f & EPI_TRANSPOSE)) {
-            float4* dst = reinterpret_cast<float4*>(P.c + static_cast<size_t>(r) * P.ldc + c0);
-#pragma unroll
-            for (int q = 0; q < 4; ++q)
-                dst[q] = make_float4(out[4 * q], out[4 * q + 1], out[4 * q + 2], out[4 * q + 3]);
-        } else if (f & EPI_TRANSPOSE) {
-            // lanes hold consecutive rows -> each transposed column store is coalesced
-#pragma unroll
-            for (int j = 0; j < 16; ++j)
-                if (c0 + j < P.cols) P.c[static_cast<size_t>(c0 + j) * P.ldc + r] = out[j];
-        } else {
-#pragma unroll
-            for (int j = 0; j < 16; ++j)
-                if (c0 + j < P.cols) P.c[static_cast<size_t>(r) * P.ldc + c0 + j] = out[j];
-        }
-        if (mirror) {
-#pragma unroll
-            for (int j = 0; j < 16; ++j)
-                if (c0 + j < P.cols) P.c[static_cast<size_t>(c0 + j) * P.ldc + r] = out[j];
-        }
-        if (f & EPI_ALSO_T) {
-#pragma unroll
-            for (int j = 0; j < 16; ++j)
-                if (c0 + j < P.cols) P.c_t[static_cast<size_t>(c0 + j) * P.ldc_t + r] = out[j];
-        }
-    }
+    epilogue_chunks<kFmt>(P, tm, tn, tmem + (static_cast<uint32_t>(warp * 32) << 16),
+                          tm * kTile + warp * 32 + static_cast<int>(lane), col_scale, 0, kTile / 16, have_acc);
 
     PF_GSTAMP(5, threadIdx.x == 0);
     ptx::tc_fence_before();

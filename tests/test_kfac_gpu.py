@@ -248,3 +248,76 @@ def test_ngd_step_matches_reference(K):
     assert rel_fro(delta, w_ref - w_before) <= 1e-4
     K.ngd_step([w], st, [g])
     assert st.staleness == [2]
+
+
+@pytest.fixture
+def persistent(K):
+    """Run the damped inverse through the persistent task-graph executor
+    (pf_set_inverse_mode(1)) for the duration of one test."""
+    lib = K.L.lib()
+    K.L.check(lib.pf_set_inverse_mode(1), "mode")
+    yield
+    K.L.check(lib.pf_set_inverse_mode(0), "mode")
+
+
+def _mixed_batch(K, sizes, seed0):
+    ms = [spd(seed0 + i, d) for i, d in enumerate(sizes)]
+    ts = [torch.from_numpy(m).float().cuda() for m in ms]
+    outs = [torch.empty_like(t) for t in ts]
+    digits = [torch.empty(K.slice_bytes(t.shape[0], t.shape[0]), dtype=torch.uint8, device="cuda") for t in ts]
+    return ms, ts, outs, digits
+
+
+@pytest.mark.parametrize("sizes", [(1,), (100,), (128, 129), (256, 300, 300), (64, 768, 768, 1024), (2048, 512)])
+def test_persistent_executor_bit_identical(K, sizes):
+    """The persistent task-graph executor runs the same arithmetic as the
+    per-step launches: inverses and digit forms are bit-identical."""
+    ms, ts, outs, digits = _mixed_batch(K, sizes, 70)
+    K.damped_inverse_batched(ts, 0.1, outs, digits)
+    ref = [(o.clone(), dg.clone()) for o, dg in zip(outs, digits)]
+    lib = K.L.lib()
+    K.L.check(lib.pf_set_inverse_mode(1), "mode")
+    try:
+        for o in outs:
+            o.fill_(float("nan"))
+        K.damped_inverse_batched(ts, 0.1, outs, digits)
+        K.damped_inverse_batched(ts, 0.1, outs, digits)  # cached program, counters reset
+    finally:
+        K.L.check(lib.pf_set_inverse_mode(0), "mode")
+    for (o_ref, d_ref), o, dg, m in zip(ref, outs, digits, ms):
+        assert torch.equal(o, o_ref)
+        assert torch.equal(dg, d_ref)
+        m32 = m.astype(np.float32).astype(np.float64)
+        assert residual(m32, o.double().cpu().numpy(), 0.1) <= INV_RESIDUAL_TOL
+
+
+def test_persistent_executor_not_pd(K, persistent):
+    m = torch.tensor([[1.0, 2.0], [2.0, 1.0]], device="cuda")
+    with pytest.raises(K.NotPositiveDefinite) as e:
+        K.cholesky_spd_inverse(m, 0.0)
+    assert e.value.column == 2
+    m = np.eye(300)
+    m[170, 170] = -1.0
+    with pytest.raises(K.NotPositiveDefinite) as e:
+        K.cholesky_spd_inverse(torch.from_numpy(m).float().cuda(), 0.5)
+    assert e.value.column == 171
+
+
+def test_persistent_executor_in_cuda_graph(K, persistent):
+    _, ts, outs, digits = _mixed_batch(K, (512, 256), 90)
+    K.damped_inverse_batched(ts, 0.1, outs, digits, check=False)
+    torch.cuda.synchronize()
+    want = [o.clone() for o in outs]
+    s = torch.cuda.Stream()
+    s.wait_stream(torch.cuda.current_stream())
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.stream(s):
+        with torch.cuda.graph(g, stream=s):
+            K.damped_inverse_batched(ts, 0.1, outs, digits, check=False)
+    for o in outs:
+        o.zero_()
+    g.replay()
+    g.replay()
+    torch.cuda.synchronize()
+    for o, w in zip(outs, want):
+        assert torch.equal(o, w)
