@@ -408,18 +408,6 @@ PIPELINE_LADDER = {  # SURVEY §8d 1/2/4/8-GPU ladder (BERT-Large, micro-batch 3
 }
 
 
-def pipeline_costs(cfg, layers_per_stage):
-    """CostTable for the assigner from this build's measured kernel rates
-    (DESIGN.md §3): F = l x 105 GFLOP at ~600 TFLOP/s, B = 2F, one set's SYRK
-    per micro-batch ~0.1 ms, one set's inversion ~3.2 ms, precondition
-    ~0.6 ms per encoder layer."""
-    from paper_2211_14133_b200 import schedule as S
-    spd = 2 if cfg.method == S.Method.Chimera else 1
-    t_f = layers_per_stage * 0.175
-    return S.CostTable(t_f=t_f, t_b=2 * t_f, t_curv=0.1, t_inv=layers_per_stage * 3.2,
-                       t_prec=spd * layers_per_stage * 0.6)
-
-
 def pipeline_section(args, rank, world, local_rank, dist):
     import torch
     from paper_2211_14133_b200 import schedule as S
@@ -434,14 +422,22 @@ def pipeline_section(args, rank, world, local_rank, dist):
     L = bert.layers // spec["stages"]
     cfg = S.PipelineConfig(method=method, stages=spec["stages"], micro_batches=spec["micro_batches"],
                            micro_batch_size=32, replicas=spec["replicas"], layers_per_stage=L, seq_len=128)
-    costs = pipeline_costs(cfg, L)
+    costs_box = {"costs": "measured"}  # profiler -> CostTable closed loop (engine.measure_stage_times)
     out = {"model": "BERT-Large (24 x 1024, FFN 4096, 16 heads), random init", "method": spec["method"],
            "stages": cfg.stages, "micro_batches": cfg.micro_batches, "micro_batch": "32 x 128",
            "replicas": cfg.replicas, "layers_per_stage": L, "data": "synthetic token ids, 15% MLM"}
 
     def measure(kfac):
         t = PipeFisherTrainer(cfg, bert, rank, world, torch.device("cuda", local_rank), kfac=kfac,
-                              refresh=2, costs=costs, dist=dist, seed=11)
+                              refresh=2, costs=costs_box["costs"], dist=dist, seed=11)
+        if t.measured is not None:
+            m = t.measured
+            costs_box["costs"] = t.costs
+            costs_box["measured"] = {"t_f_ms": m.f, "t_b_ms": m.b, "curvature_item_ms": m.curv,
+                                     "inversion_item_ms": m.inv, "precondition_stage_ms": m.prec,
+                                     "cost_table": {k: getattr(t.costs, k) for k in
+                                                    ("t_f", "t_b", "t_curv", "t_inv", "t_prec")},
+                                     "source": "CUDA events on this GPU, median of 3, max over ranks"}
         t.run_cycle()  # warm-up (allocations, cuBLAS heuristics)
         if dist: dist.barrier()
         res = [t.run_cycle(record=(i == 1)) for i in range(2)]
@@ -461,13 +457,15 @@ def pipeline_section(args, rank, world, local_rank, dist):
         return step, util, loss, info
 
     try:
-        plain_ms, plain_util, _, _ = measure(False)
-        step_ms, util, loss, info = measure(True)
+        step_ms, util, loss, info = measure(True)   # measures the cost table first
+        plain_ms, plain_util, _, _ = measure(False)  # same schedule costs, K-FAC items dropped
         seqs = cfg.micro_batches * cfg.micro_batch_size * cfg.groups() * (2 if spd == 2 else 1) / spd
         out.update({"step_ms": step_ms, "plain_step_ms": plain_ms, "step_ratio_vs_plain": step_ms / plain_ms,
                     "gpu_util": util, "plain_gpu_util": plain_util,
                     "sequences_per_s": seqs / (step_ms * 1e-3), "loss": loss, **info,
                     "util_definition": "union of F/B/K-FAC/collective op intervals (CUDA events) / cycle wall time, min over ranks"})
+        if "measured" in costs_box:
+            out["measured_costs"] = costs_box["measured"]
     except Exception as e:  # reported, never fatal for the bench line
         out["error"] = f"{type(e).__name__}: {e}"[:400]
     return out

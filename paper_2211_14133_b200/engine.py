@@ -297,6 +297,94 @@ class CudaBackend:
             mod.store.clear()
 
 
+# ------------------------------------------------------------ measured costs
+@dataclass
+class MeasuredTimes:
+    """Per-item device times (ms, CUDA events on the launching stream) of one
+    hosted stage, the inputs of the assigner's CostTable."""
+    f: float             # forward of one micro-batch (tape capture on)
+    b: float             # backward of one micro-batch
+    curv: float          # one curvature item: one layer's A- or B-set SYRKs, one micro-batch (max of the two)
+    inv: float           # one inversion item: one layer's A- or B-set damped inverses (max of the two)
+    prec: float          # precondition + update of the whole stage
+    layers: int          # encoder layers per stage (l)
+    stages_per_device: int
+    param_bytes: int     # fp32 parameters of the stage (SyncGrad volume)
+    factor_bytes: int    # fp32 factors of the stage (SyncCurvature volume)
+
+
+def costs_from_times(t: MeasuredTimes, comm_alpha_ms: float = 0.01,
+                     comm_bytes_per_ms: float = 3.0e8) -> S.CostTable:
+    """Reference cost-table semantics: t_curv is
+    charged per (layer, set, micro) item; an inversion item lasts t_inv / l,
+    so t_inv = l x one set's inversion; t_prec is the per-DEVICE tail, split
+    t_prec / spd per hosted stage.  Collective costs: alpha-beta model with
+    the given NVLink estimates (bubblefill model_collective)."""
+    return S.CostTable(t_f=t.f, t_b=t.b, t_curv=t.curv, t_inv=t.layers * t.inv,
+                       t_prec=t.stages_per_device * t.prec, m_theta=t.param_bytes,
+                       m_curv=t.factor_bytes, comm_alpha=comm_alpha_ms, comm_beta=comm_bytes_per_ms)
+
+
+def measure_stage_times(backend: "CudaBackend", reps: int = 3) -> MeasuredTimes:
+    """Time the work items of this rank's first hosted stage.  Mutates the
+    backend's model and K-FAC state: use a throw-away backend."""
+    stage = min(backend.stages)
+    mod, ks = backend.stages[stage], backend.kstate[stage]
+    topo = backend.topo
+    micro = next(m for m in range(topo.cfg.micro_batches)
+                 if topo.device(topo.pipe_of(m), stage, backend.rank // topo.D) == backend.rank)
+
+    def timed(fn, stream):
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        fn()
+        e1.record(stream)
+        return e0, e1
+
+    def median_ms(pairs):
+        torch.cuda.synchronize(backend.device)
+        v = sorted(a.elapsed_time(b) for a, b in pairs)
+        return v[len(v) // 2]
+
+    x = None if mod.is_first else torch.randn((backend.B, backend.Sq, backend.bert.hidden), device=backend.device,
+                                              dtype=torch.bfloat16)
+    gy = None if mod.is_last else torch.randn((backend.B, backend.Sq, backend.bert.hidden), device=backend.device,
+                                              dtype=torch.bfloat16)
+    fwd, bwd = [], []
+    for i in range(reps + 1):  # first round warms cuBLAS / allocator
+        pf = timed(lambda: backend.forward(stage, micro, None if x is None else x.clone(), True, 0), backend.compute)
+        pb = timed(lambda: backend.backward(stage, micro, gy, True), backend.compute)
+        if i:
+            fwd.append(pf)
+            bwd.append(pb)
+        for p in mod.parameters():
+            p.grad = None
+    curv, inv = [], []
+    for i in range(reps + 1):
+        for f in (0, 1):
+            pc = timed(lambda: backend.curvature_many([(stage, 0, f, micro)], None), backend.kfac_stream)
+            pi = timed(lambda: backend.invert_many([(stage, 0, f)], None), backend.kfac_stream)
+            if i:
+                curv.append(pc)
+                inv.append(pi)
+    t_curv = median_ms(curv[0::2]), median_ms(curv[1::2])
+    t_inv = median_ms(inv[0::2]), median_ms(inv[1::2])
+    prec = []
+    for i in range(reps + 1):
+        backend.forward(stage, micro, None if x is None else x.clone(), False, 0)
+        backend.backward(stage, micro, gy, False)
+        pp = timed(lambda: backend.precondition(stage, 0), backend.compute)
+        if i:
+            prec.append(pp)
+    backend.end_cycle()
+    backend.losses.clear()
+    params = sum(p.numel() for p in mod.parameters()) * 4
+    factors = sum(t.numel() for t in ks.factor.values()) * 4
+    return MeasuredTimes(f=median_ms(fwd), b=median_ms(bwd), curv=max(t_curv), inv=max(t_inv),
+                         prec=median_ms(prec), layers=topo.cfg.layers_per_stage,
+                         stages_per_device=len(backend.stages), param_bytes=params, factor_bytes=factors)
+
+
 @dataclass
 class CycleResult:
     cycle_ms: float
@@ -318,6 +406,12 @@ class PipeFisherTrainer:
         if self.topo.n_devices() != world:
             raise ValueError(f"config needs {self.topo.n_devices()} devices, world is {world}")
         self.device = device or torch.device("cuda", torch.cuda.current_device())
+        self.measured: Optional[MeasuredTimes] = None
+        if isinstance(costs, str):
+            if costs != "measured":
+                raise ValueError("costs: a CostTable or 'measured'")
+            costs = self._measure_costs(damping, lr, seed, dist)
+        self.costs = costs
         self.backend = CudaBackend(self.topo, bert, rank, self.device, kfac, damping, lr, seed)
         self.filled = None
         if cfg.stages == 1 and cfg.replicas == 1:
@@ -342,6 +436,26 @@ class PipeFisherTrainer:
             self.comm = R.Comm(dist, rank, R.channel_plan(progs), replica_sets, self.device)
         self.executor = R.Executor(self.program, self.backend, self.comm or _LocalComm(), rank)
         self.cycles = 0
+
+    def _measure_costs(self, damping, lr, seed, dist) -> S.CostTable:
+        """Profiler -> CostTable closed loop (the paper's 'collect the profile,
+        then pick one work from the queue'): time the work
+        items on a throw-away backend, take the max over ranks (every rank
+        must build the identical schedule), convert to the reference's
+        cost-table semantics."""
+        probe = CudaBackend(self.topo, self.bert, self.rank, self.device, True, damping, lr, seed)
+        t = measure_stage_times(probe)
+        del probe
+        torch.cuda.empty_cache()
+        if dist is not None and self.world > 1:
+            v = torch.tensor([t.f, t.b, t.curv, t.inv, t.prec, float(t.stages_per_device),
+                              float(t.param_bytes), float(t.factor_bytes)], device=self.device, dtype=torch.float64)
+            dist.all_reduce(v, op=dist.ReduceOp.MAX)
+            t = MeasuredTimes(*[float(a) for a in v[:5].tolist()], layers=t.layers,
+                              stages_per_device=int(v[5]), param_bytes=int(v[6]), factor_bytes=int(v[7]))
+        self.measured = t
+        torch.cuda.set_stream(torch.cuda.default_stream(self.device))
+        return costs_from_times(t)
 
     def run_cycle(self, record: bool = False) -> CycleResult:
         b = self.backend

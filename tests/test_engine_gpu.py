@@ -88,3 +88,16 @@ def test_plain_pipeline_baseline_has_no_kfac_ops():
     assert {o.kind for o in t.program} <= {"F", "B", "SYNC_GRAD", "PREC"}
     r = t.run_cycle(record=True)
     assert torch.isfinite(torch.tensor(r.loss))
+
+
+def test_measured_cost_table_closed_loop():
+    """costs='measured': the work items are timed on this GPU and the cost
+    table the assigner sees is built from them."""
+    from paper_2211_14133_b200.engine import PipeFisherTrainer
+    cfg = S.PipelineConfig(stages=1, micro_batches=2, micro_batch_size=4, seq_len=64, layers_per_stage=2)
+    t = PipeFisherTrainer(cfg, small(), kfac=True, refresh=2, costs="measured", damping=0.1, lr=1e-2, seed=3)
+    m = t.measured
+    assert m is not None and min(m.f, m.b, m.curv, m.inv, m.prec) > 0.0
+    assert t.costs.t_inv == pytest.approx(2 * m.inv) and t.costs.t_curv == m.curv
+    r = t.run_cycle(record=True)
+    assert torch.isfinite(torch.tensor(r.loss))

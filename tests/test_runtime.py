@@ -213,3 +213,22 @@ def test_gloo_execution_no_deadlock_and_data_routed(method, D, N, W, L, inv_par)
         syncs = [e for e in logs[r] if e[0] == "SYNC_CURV"]
         if W > 1 or method == S.Method.Chimera:
             assert syncs and all(e[-1] > 0 for e in syncs)  # every replica joined
+
+
+def test_measured_costs_follow_reference_semantics():
+    """engine.costs_from_times: t_curv per (layer, set, micro) item, t_inv =
+    l x one set's inversion (items last t_inv / l), t_prec = per-device tail
+    (spd x stage), collective volumes from the stage's bytes."""
+    from paper_2211_14133_b200.engine import MeasuredTimes, costs_from_times
+    t = MeasuredTimes(f=0.5, b=1.0, curv=0.1, inv=2.0, prec=0.3, layers=3, stages_per_device=2,
+                      param_bytes=10 ** 8, factor_bytes=4 * 10 ** 8)
+    c = costs_from_times(t)
+    assert (c.t_f, c.t_b, c.t_curv, c.t_inv, c.t_prec) == (0.5, 1.0, 0.1, 6.0, 0.6)
+    assert c.m_theta == 10 ** 8 and c.m_curv == 4 * 10 ** 8
+    cfg = S.PipelineConfig(method=S.Method.GPipe, stages=4, micro_batches=4, replicas=1, layers_per_stage=3)
+    q = S.enumerate_kfac_works(cfg, c)
+    inv = [w for w in q.items if w.kind == S.WorkKind.Inversion]
+    assert inv and all(abs(w.duration - c.t_inv / 3) < 1e-12 for w in inv)
+    base = S.build_schedule(cfg, c)
+    filled = S.assign_works(base, cfg, c, q, S.AssignOptions())
+    assert filled.refresh_period >= 1
