@@ -267,7 +267,7 @@ void launch_gemms(const std::vector<GemmSpec>& specs, cudaStream_t stream) {
         batch.n_probs = probs;
         batch.total_tiles = tiles;
         if (tiles == 0) continue;
-        launch(kernel, dim3(tiles), dim3(128), T::kSmemBytes, stream, batch);
+        launch(kernel, dim3(tiles), dim3(T::kThreads), T::kSmemBytes, stream, batch);
         after_launch("umma_gemm_kernel");
     }
 }

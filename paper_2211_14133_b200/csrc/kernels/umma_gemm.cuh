@@ -104,6 +104,9 @@ struct GemmTraits {
     static constexpr int kKSteps = kFmt == kOZ8 ? 2 : 4;  // 32-byte UMMA k-steps per block
     static constexpr uint32_t kTmemCols = kFmt == kOZ8 ? 512 : 128;
     static constexpr int kMinBlocks = kFmt == kOZ8 ? 1 : 2;
+    // kOZ8 (one CTA per SM: 512 TMEM columns) runs 8 warps so the 4-accumulator
+    // epilogue is split over warp pairs sharing a TMEM lane quarter
+    static constexpr int kThreads = kFmt == kOZ8 ? 256 : 128;
     // kind::i8: signed int8 A/B (format 1), s32 accumulate (c_format 2)
     static constexpr uint32_t kIdesc =
         kFmt == kOZ8 ? ((2u << 4) | (1u << 7) | (1u << 10) | ((128u >> 3) << 17) | ((128u >> 4) << 24))
@@ -236,7 +239,7 @@ __device__ __forceinline__ void epilogue_chunks(const GemmDesc& P, int tm, int t
 }
 
 template <int kFmt>
-__global__ void __launch_bounds__(128, GemmTraits<kFmt>::kMinBlocks)
+__global__ void __launch_bounds__(GemmTraits<kFmt>::kThreads, GemmTraits<kFmt>::kMinBlocks)
     umma_gemm_kernel(const __grid_constant__ GemmBatch batch) {
     using T = GemmTraits<kFmt>;
     constexpr int kStages = T::kStages;
@@ -288,10 +291,6 @@ __global__ void __launch_bounds__(128, GemmTraits<kFmt>::kMinBlocks)
         ptx::prefetch_tmap(&batch.maps[P.b_map]);
     }
     ptx::grid_dep_wait();  // operands, scales and C come from earlier launches
-    if constexpr (kFmt == kOZ8) {
-        const int c = tn * kTile + static_cast<int>(threadIdx.x);
-        col_scale[threadIdx.x] = c < P.cols ? ptx::pow2f(P.b_exp[c]) : 0.0f;
-    }
     ptx::tc_fence_before();
     __syncthreads();
     ptx::tc_fence_after();
@@ -364,6 +363,14 @@ __global__ void __launch_bounds__(128, GemmTraits<kFmt>::kMinBlocks)
         PF_GSTAMP(3, true);
     }
     __syncwarp();
+    if constexpr (kFmt == kOZ8) {  // warps 2-5: column scales while the MMAs run
+        const int t = static_cast<int>(threadIdx.x) - 64;
+        if (t >= 0 && t < kTile) {
+            const int c = tn * kTile + t;
+            col_scale[t] = c < P.cols ? ptx::pow2f(__ldcg(P.b_exp + c)) : 0.0f;
+        }
+        __syncthreads();
+    }
 
     // ---------------- epilogue: TMEM -> registers -> global
     const bool have_acc = kb1 > kb0;
@@ -374,8 +381,14 @@ __global__ void __launch_bounds__(128, GemmTraits<kFmt>::kMinBlocks)
     PF_GSTAMP(4, threadIdx.x == 0);
     ptx::grid_dep_launch();  // main loop done: let the next launch start its prologue
     __syncwarp();
-    epilogue_chunks<kFmt>(P, tm, tn, tmem + (static_cast<uint32_t>(warp * 32) << 16),
-                          tm * kTile + warp * 32 + static_cast<int>(lane), col_scale, 0, kTile / 16, have_acc);
+    {
+        constexpr int kPairs = T::kThreads / 128;  // warps sharing a TMEM lane quarter
+        const int ew = warp & 3, part = warp >> 2;
+        constexpr int kChunks = kTile / 16 / kPairs;
+        epilogue_chunks<kFmt>(P, tm, tn, tmem + (static_cast<uint32_t>(ew * 32) << 16),
+                              tm * kTile + ew * 32 + static_cast<int>(lane), col_scale, part * kChunks,
+                              (part + 1) * kChunks, have_acc);
+    }
 
     PF_GSTAMP(5, threadIdx.x == 0);
     ptx::tc_fence_before();
