@@ -56,12 +56,14 @@ constexpr int kMaxLeafBatch = 32;
 constexpr int kLeafPitch = 129;   // Ls: active trailing matrix (column walks conflict-free)
 constexpr int kXPitch = 132;      // Xs, PT: float4 rows
 constexpr int kSmallPitch = 36;   // LT, XTd: transposed 32x32 diagonal blocks
-constexpr int kTPitch = 100;      // Tb: T_p, 32 x (<= 96)
+// Tb: T_1, T_2, T_3 (32 x 32bi, pitch 32bi + 4), accumulated panel by panel
+__host__ __device__ constexpr int t_pitch(int bi) { return 32 * bi + 4; }
+__host__ __device__ constexpr int t_offset(int bi) { return bi == 1 ? 0 : bi == 2 ? 32 * t_pitch(1) : 32 * (t_pitch(1) + t_pitch(2)); }
 constexpr int kLsFloats = kLeaf * kLeafPitch + 4 - (kLeaf * kLeafPitch) % 4;
 constexpr int kXsFloats = kLeaf * kXPitch;
 constexpr int kPTFloats = 32 * kXPitch;
 constexpr int kSmallFloats = 32 * kSmallPitch;
-constexpr int kTbFloats = 32 * kTPitch;
+constexpr int kTbFloats = 32 * (t_pitch(1) + t_pitch(2) + t_pitch(3));
 constexpr int kLeafSmemFloats =
     kLsFloats + kXsFloats + 3 * kPTFloats + 2 * kSmallFloats + kTbFloats + 64 + kLeaf + 4;
 constexpr int kLeafSmemBytes = kLeafSmemFloats * 4;
@@ -241,28 +243,41 @@ __device__ __forceinline__ void trail_tile(float* Ls, const float* PTp, int r0, 
             }
 }
 
-// T_p tile (ti in [0,8), tj in [0, 8p)): T[i][j] = sum_{k} L[32p+i][k] X[k][j],
-// k from 4tj (X is lower triangular) to 32p, L rows read from the panels PT_q.
-__device__ __forceinline__ void tprod_tile(const float* PT, const float* Xs, float* Tb, int p, int ti, int tj) {
+// Contribution of panel q to T_bi (bi > q), tile (ti in [0,8), tj in [0, 8(q+1))):
+//   T_bi[i][j] += sum_{k in panel q, k >= 4tj} L[32bi+i][k] X[k][j]
+// The first panel that reaches column j initialises the tile; later panels
+// continue the same fmaf chain (k ascending), so the result is bit-identical
+// to one pass over k in [4tj, 32bi).
+__device__ __forceinline__ void tpanel_tile(const float* PT, const float* Xs, float* Tb, int bi, int q, int ti,
+                                            int tj) {
+    float* T = Tb + t_offset(bi);
+    const int tp = t_pitch(bi);
     float acc[4][4];
-    zero4x4(acc);
     const int kstart = 4 * tj;
-    for (int q = kstart / 32; q < p; ++q) {
-        const int k0 = max(kstart - 32 * q, 0);
-        outer4(acc, PT + q * kPTFloats + 32 * p + 4 * ti, kXPitch, Xs + (32 * q) * kXPitch + 4 * tj, kXPitch,
-               k0, 32);
+    if (kstart / 32 == q) {
+        zero4x4(acc);
+    } else {
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+            const float4 v = *reinterpret_cast<const float4*>(T + (4 * ti + u) * tp + 4 * tj);
+            acc[u][0] = v.x;
+            acc[u][1] = v.y;
+            acc[u][2] = v.z;
+            acc[u][3] = v.w;
+        }
     }
+    outer4(acc, PT + q * kPTFloats + 32 * bi + 4 * ti, kXPitch, Xs + (32 * q) * kXPitch + 4 * tj, kXPitch,
+           max(kstart - 32 * q, 0), 32);
 #pragma unroll
     for (int u = 0; u < 4; ++u)
-        *reinterpret_cast<float4*>(Tb + (4 * ti + u) * kTPitch + 4 * tj) =
-            make_float4(acc[u][0], acc[u][1], acc[u][2], acc[u][3]);
+        *reinterpret_cast<float4*>(T + (4 * ti + u) * tp + 4 * tj) = make_float4(acc[u][0], acc[u][1], acc[u][2], acc[u][3]);
 }
 
 // X[32p+i][j] = -sum_{k <= i} X_pp[i][k] T[k][j]  for the 4x4 tile (ti, tj)
 __device__ __forceinline__ void xprod_tile(const float* XTd, const float* Tb, float* Xs, int p, int ti, int tj) {
     float acc[4][4];
     zero4x4(acc);
-    outer4(acc, XTd + 4 * ti, kSmallPitch, Tb + 4 * tj, kTPitch, 0, 4 * ti + 4);
+    outer4(acc, XTd + 4 * ti, kSmallPitch, Tb + t_offset(p) + 4 * tj, t_pitch(p), 0, 4 * ti + 4);
 #pragma unroll
     for (int u = 0; u < 4; ++u)
         *reinterpret_cast<float4*>(Xs + (32 * p + 4 * ti + u) * kXPitch + 4 * tj) =
@@ -307,6 +322,29 @@ __device__ __forceinline__ void load_lower(float* dst, const float* src, int ld,
     }
 }
 
+// vectorised full-block load split in two: issue (registers) and commit (smem)
+constexpr int kLoadPer = kLeaf * kLeaf / 4 / kLeafThreads;  // 16 float4 per thread
+__device__ __forceinline__ void load_lower_issue(const float* src, int ld, float4 (&v)[kLoadPer]) {
+#pragma unroll
+    for (int q = 0; q < kLoadPer; ++q) {
+        const int idx = threadIdx.x + q * kLeafThreads;
+        const int r = idx / (kLeaf / 4), c = 4 * (idx % (kLeaf / 4));
+        v[q] = (c <= r) ? __ldcg(reinterpret_cast<const float4*>(src + (size_t)r * ld + c)) : make_float4(0.f, 0.f, 0.f, 0.f);
+    }
+}
+__device__ __forceinline__ void load_lower_commit(float* dst, const float4 (&v)[kLoadPer]) {
+#pragma unroll
+    for (int q = 0; q < kLoadPer; ++q) {
+        const int idx = threadIdx.x + q * kLeafThreads;
+        const int r = idx / (kLeaf / 4), c = 4 * (idx % (kLeaf / 4));
+        float* d = dst + r * kLeafPitch + c;
+        d[0] = c <= r ? v[q].x : 0.f;
+        d[1] = c + 1 <= r ? v[q].y : 0.f;
+        d[2] = c + 2 <= r ? v[q].z : 0.f;
+        d[3] = c + 3 <= r ? v[q].w : 0.f;
+    }
+}
+
 // zero the strictly-upper 32x32 blocks of Xs (never written otherwise)
 __device__ __forceinline__ void zero_upper_blocks(float* Xs) {
     for (int idx = threadIdx.x; idx < kLeaf * kLeaf / 4; idx += kLeafThreads) {
@@ -317,21 +355,40 @@ __device__ __forceinline__ void zero_upper_blocks(float* Xs) {
 }
 
 // x = X (lower, zeros above) and xt = X^T for the n x n block
-__device__ __forceinline__ void store_x(const float* Xs, float* x, float* xt, int ld, int n) {
+// `tbuf` (pitch kLeafPitch, 128 rows) is scratch: the active-matrix buffer,
+// free once the factorisation is done.  Every thread must call this.
+__device__ __forceinline__ void store_x(const float* Xs, float* tbuf, float* x, float* xt, int ld, int n) {
     const int tid = threadIdx.x;
     const bool vec = n == kLeaf && (ld % 4 == 0) && ((reinterpret_cast<uintptr_t>(x) & 15) == 0) &&
                      ((reinterpret_cast<uintptr_t>(xt) & 15) == 0);
     if (vec) {
-        for (int idx = tid; idx < kLeaf * kLeaf / 4; idx += kLeafThreads) {
-            const int r = idx / (kLeaf / 4), c = 4 * (idx % (kLeaf / 4));
-            *reinterpret_cast<float4*>(x + (size_t)r * ld + c) =
-                *reinterpret_cast<const float4*>(Xs + r * kXPitch + c);
+        // shared-memory reads of a batch first, then its global stores
+#pragma unroll
+        for (int b = 0; b < 2; ++b) {
+            float4 v[8];
+#pragma unroll
+            for (int q = 0; q < 8; ++q) {
+                const int idx = tid + (8 * b + q) * kLeafThreads;
+                const int r = idx / (kLeaf / 4), c = 4 * (idx % (kLeaf / 4));
+                v[q] = *reinterpret_cast<const float4*>(Xs + r * kXPitch + c);
+            }
+#pragma unroll
+            for (int q = 0; q < 8; ++q) {
+                const int idx = tid + (8 * b + q) * kLeafThreads;
+                const int r = idx / (kLeaf / 4), c = 4 * (idx % (kLeaf / 4));
+                *reinterpret_cast<float4*>(x + (size_t)r * ld + c) = v[q];
+            }
         }
-        for (int idx = tid; idx < kLeaf * kLeaf / 4; idx += kLeafThreads) {
-            const int r = idx % kLeaf, c = 4 * (idx / kLeaf);  // lanes: consecutive r (conflict-free)
-            *reinterpret_cast<float4*>(xt + (size_t)r * ld + c) =
-                make_float4(Xs[c * kXPitch + r], Xs[(c + 1) * kXPitch + r], Xs[(c + 2) * kXPitch + r],
-                            Xs[(c + 3) * kXPitch + r]);
+        // X^T: transpose into the (now free) pitch-129 buffer, then store its rows
+        for (int idx = tid; idx < kLeaf * kLeaf; idx += kLeafThreads) {
+            const int r = idx / kLeaf, c = idx % kLeaf;  // lanes: consecutive c
+            tbuf[c * kLeafPitch + r] = Xs[r * kXPitch + c];
+        }
+        __syncthreads();
+#pragma unroll 4
+        for (int idx = tid; idx < kLeaf * kLeaf; idx += kLeafThreads) {
+            const int r = idx / kLeaf, c = idx % kLeaf;
+            xt[(size_t)r * ld + c] = tbuf[r * kLeafPitch + c];
         }
     } else {
         for (int idx = tid; idx < n * n; idx += kLeafThreads) {
@@ -370,10 +427,17 @@ __device__ __forceinline__ void leaf_body(const LeafArgs& A, float* leaf_smem, b
 
     PF_STAMP(0);
     if (tid == 0) *bad = INT_MAX;
-    zero_upper_blocks(Xs);
-    PF_STAMP(1);
     if (pdl) ptx::grid_dep_wait();  // PDL: A is produced by the previous launch
-    load_lower(Ls, A.a, A.ld, A.n);
+    const bool vec = A.n == kLeaf && (A.ld % 4 == 0) && ((reinterpret_cast<uintptr_t>(A.a) & 15) == 0);
+    if (vec) {
+        float4 v[kLoadPer];
+        load_lower_issue(A.a, A.ld, v);  // global loads in flight ...
+        zero_upper_blocks(Xs);           // ... while the upper blocks of X are cleared
+        load_lower_commit(Ls, v);
+    } else {
+        zero_upper_blocks(Xs);
+        load_lower(Ls, A.a, A.ld, A.n);
+    }
     __syncthreads();
     PF_STAMP(2);
 
@@ -383,17 +447,19 @@ __device__ __forceinline__ void leaf_body(const LeafArgs& A, float* leaf_smem, b
         if (warp == 0) {
             chol32(Ls, LT, rdiag, lbuf, c0, A.n, A.col0, bad);
         } else if (p > 0) {
+            // rest of U(p-1) + panel p-1's contribution to T_p (the later T_bi
+            // get theirs on the idle warps of phase B)
             const int base = 8 * (p + 1), m = 32 - base;  // tile rows/cols [base, 32), lower
             const int nrest = m * (m + 1) / 2;
-            const int ntp = 64 * p;
-            for (int t = tid - 32; t < nrest + ntp; t += kLeafThreads - 32) {
+            const int per = 64 * p;                       // tiles of one T_bi slice (8 x 8p)
+            for (int t = tid - 32; t < nrest + per; t += kLeafThreads - 32) {
                 if (t < nrest) {
                     int i, j;
                     lower_pair(t, i, j);
                     trail_tile(Ls, PT + (p - 1) * kPTFloats, 4 * (base + i), 4 * (base + j));
                 } else {
-                    const int u = t - nrest;
-                    tprod_tile(PT, Xs, Tb, p, u / (8 * p), u % (8 * p));
+                    const int v = t - nrest;
+                    tpanel_tile(PT, Xs, Tb, p, p - 1, v / (8 * p), v % (8 * p));
                 }
             }
         }
@@ -402,8 +468,18 @@ __device__ __forceinline__ void leaf_body(const LeafArgs& A, float* leaf_smem, b
         if (p == 3) break;
         // ---- B: TRSM of the rows below || X_pp
         const int below = kLeaf - c0 - 32;
-        if (tid < below) trsm_row(Ls, LT, rdiag, PT + p * kPTFloats, c0, c0 + 32 + tid);
-        if (warp == kLeafWarps - 1) inv32(LT, rdiag, Xs, XTd, c0);
+        if (tid < below) {
+            trsm_row(Ls, LT, rdiag, PT + p * kPTFloats, c0, c0 + 32 + tid);
+        } else if (warp == kLeafWarps - 1) {
+            inv32(LT, rdiag, Xs, XTd, c0);
+        } else if (p > 0) {  // warps between: panel p-1's contribution to T_{p+1} .. T_3
+            const int first = (below + 31) / 32 * 32;  // first thread of the free warps
+            const int per = 64 * p, n = per * (3 - p);
+            for (int t = tid - first; t >= 0 && t < n; t += (kLeafWarps - 1) * 32 - first) {
+                const int bi = p + 1 + t / per, v = t % per;
+                tpanel_tile(PT, Xs, Tb, bi, p - 1, v / (8 * p), v % (8 * p));
+            }
+        }
         __syncthreads();
         PF_STAMP(4 + 3 * p);
         // ---- C: U(p) on block column p+1 || X[p, 0:p] = -X_pp T_p
@@ -431,7 +507,7 @@ __device__ __forceinline__ void leaf_body(const LeafArgs& A, float* leaf_smem, b
     __syncthreads();
     PF_STAMP(14);
     if (pdl) ptx::grid_dep_launch();
-    store_x(Xs, A.x, A.xt, A.ld, A.n);
+    store_x(Xs, Ls, A.x, A.xt, A.ld, A.n);
     PF_STAMP(19);
     if (tid == 0) report_bad(A.info, *bad);
 }
