@@ -309,19 +309,44 @@ __global__ void f32_to_bf16_kernel(const float* x, int64_t n, __nv_bfloat16* out
 // ------------------------------------------------------------ damped inverse
 // Workspace of one factor (ld = round_up(d, 4)):
 //   fp32  A (damped factor, updated in place), L (panel blocks L21),
-//         X = L^-1 (lower), XT = L^-T (upper), T (temporary)
-//   digit form  two operand slots S0, S1 sized for d x d
+//         X = L^-1 (lower), XT = L^-T (upper), T^T of every recursion depth
+//   digit form  two operand slots S0, S1 sized for d x d, plus two per depth
+//               for the side branch
 struct InvWs {
     int d = 0, ld = 0;
     float *a, *l, *x, *xt, *t;
     void* s0;
     void* s1;
+    // per-recursion-depth digit slots of the node's side branch (T^T = (L21 X11)^T
+    // runs concurrently with the recursion on A22, so nested nodes must not share)
+    void* side0[8] = {};
+    void* side1[8] = {};
+    int t_row[8] = {};  // row of w.t where the depth's T^T lives (ld = w.ld)
     int* info = nullptr;
 };
 
+// n1 bound of the internal nodes, depth by depth (left child is the larger)
+std::vector<int> node_n1_bounds(int d) {
+    std::vector<int> b;
+    for (int n = d; n > kLeaf; n = kTile * ((n + 2 * kTile - 1) / (2 * kTile))) b.push_back(kTile * ((n + 2 * kTile - 1) / (2 * kTile)));
+    if (b.size() > 8) throw std::invalid_argument("damped inverse: d too large");
+    return b;
+}
+
+// T^T of every depth, stacked: sum of the depth bounds (can exceed d: the
+// left child takes the larger part, e.g. d = 300 -> 256 + 128 rows)
+int t_rows(int d) {
+    int r = 0;
+    for (int n1 : node_n1_bounds(d)) r += n1;
+    return std::max(r, 1);
+}
+
 size_t inverse_ws_bytes(int d) {
     const size_t plane = align256(static_cast<size_t>(round_up(d, 4)) * d * sizeof(float));
-    return 5 * plane + 2 * align256(sliced_bytes(d, d));
+    const size_t tplane = align256(static_cast<size_t>(round_up(d, 4)) * t_rows(d) * sizeof(float));
+    size_t side = 0;
+    for (int n1 : node_n1_bounds(d)) side += 2 * align256(sliced_bytes(n1, n1));
+    return 4 * plane + tplane + 2 * align256(sliced_bytes(d, d)) + side;
 }
 
 InvWs carve(void* base, int d) {
@@ -329,11 +354,25 @@ InvWs carve(void* base, int d) {
     w.d = d;
     w.ld = round_up(d, 4);
     const size_t plane = align256(static_cast<size_t>(w.ld) * d * sizeof(float));
+    const size_t tplane = align256(static_cast<size_t>(w.ld) * t_rows(d) * sizeof(float));
     char* p = static_cast<char*>(base);
-    float** f[5] = {&w.a, &w.l, &w.x, &w.xt, &w.t};
-    for (int i = 0; i < 5; ++i) *f[i] = reinterpret_cast<float*>(p + i * plane);
-    w.s0 = p + 5 * plane;
-    w.s1 = p + 5 * plane + align256(sliced_bytes(d, d));
+    float** f[4] = {&w.a, &w.l, &w.x, &w.xt};
+    for (int i = 0; i < 4; ++i) *f[i] = reinterpret_cast<float*>(p + i * plane);
+    w.t = reinterpret_cast<float*>(p + 4 * plane);
+    p += 4 * plane + tplane;
+    w.s0 = p;
+    w.s1 = p + align256(sliced_bytes(d, d));
+    char* q = p + 2 * align256(sliced_bytes(d, d));
+    int row = 0;
+    const std::vector<int> b = node_n1_bounds(d);
+    for (std::size_t k = 0; k < b.size(); ++k) {
+        w.side0[k] = q;
+        q += align256(sliced_bytes(b[k], b[k]));
+        w.side1[k] = q;
+        q += align256(sliced_bytes(b[k], b[k]));
+        w.t_row[k] = row;  // T^T of a depth-k node: n1 <= b[k] rows
+        row += b[k];
+    }
     return w;
 }
 
@@ -349,7 +388,36 @@ struct Emitter {
     virtual void slices(const std::vector<SliceReq>& reqs) = 0;
     virtual void gemms(const std::vector<GemmSpec>& specs) = 0;
     virtual void leaves(const std::vector<InvWs>& ws, int o, int n) = 0;
+    // work emitted between side_begin(k) and side_end(k) may run concurrently
+    // with what follows on the main chain until side_join(k)
+    virtual void side_begin(int) {}
+    virtual void side_end(int) {}
+    virtual void side_join(int) {}
 };
+
+// Per-thread, per-device pool of (stream, done event) pairs for the side
+// branches of the recursion, indexed by (group slot, depth).
+struct SideSlot {
+    cudaStream_t stream = nullptr;
+    cudaEvent_t fork = nullptr, done = nullptr;
+};
+
+SideSlot& side_slot(int group, int depth) {
+    thread_local std::vector<std::vector<SideSlot>> pools;  // [device][group * 8 + depth]
+    int dev = 0;
+    check(cudaGetDevice(&dev), "cudaGetDevice");
+    if (pools.size() <= static_cast<std::size_t>(dev)) pools.resize(dev + 1);
+    auto& v = pools[dev];
+    const std::size_t i = static_cast<std::size_t>(group) * 8 + depth;
+    if (v.size() <= i) v.resize(i + 1);
+    SideSlot& sl = v[i];
+    if (!sl.stream) {
+        check(cudaStreamCreateWithFlags(&sl.stream, cudaStreamNonBlocking), "cudaStreamCreate(side)");
+        check(cudaEventCreateWithFlags(&sl.fork, cudaEventDisableTiming), "cudaEventCreate(side)");
+        check(cudaEventCreateWithFlags(&sl.done, cudaEventDisableTiming), "cudaEventCreate(side)");
+    }
+    return sl;
+}
 
 LeafArgs leaf_args(const InvWs& w, int o, int n) {
     return LeafArgs{at(w.a, w.ld, o, o), at(w.x, w.ld, o, o), at(w.xt, w.ld, o, o), w.info, w.ld, n, o};
@@ -362,7 +430,23 @@ SliceJob slice_job(const SliceReq& r) {
 
 struct StreamEmitter final : Emitter {
     cudaStream_t st;
-    explicit StreamEmitter(cudaStream_t s) : st(s) {}
+    cudaStream_t main;
+    int group;
+    explicit StreamEmitter(cudaStream_t s, int g = 0) : st(s), main(s), group(g) {}
+    void side_begin(int depth) override {
+        SideSlot& sl = side_slot(group, depth);
+        check(cudaEventRecord(sl.fork, main), "cudaEventRecord(side fork)");
+        check(cudaStreamWaitEvent(sl.stream, sl.fork, 0), "side fork");
+        st = sl.stream;
+    }
+    void side_end(int depth) override {
+        SideSlot& sl = side_slot(group, depth);
+        check(cudaEventRecord(sl.done, sl.stream), "cudaEventRecord(side done)");
+        st = main;
+    }
+    void side_join(int depth) override {
+        check(cudaStreamWaitEvent(main, side_slot(group, depth).done, 0), "side join");
+    }
     void damp(const std::vector<Damp2D>& jobs) override {
         DampBatch db{};
         int d = 1;
@@ -462,14 +546,14 @@ SliceReq slice_of(float* src, int ld, int r0, int c0, int rows, int k, void* slo
 //   recurse on A22
 //   T^T  = (L21 X11)^T          (via XT11)
 //   X21  = -X22 T,  XT12 = X21^T
-void inverse_rec(const std::vector<InvWs>& ws, int o, int n, Emitter& em) {
+void inverse_rec(const std::vector<InvWs>& ws, int o, int n, Emitter& em, int depth = 0) {
     if (n <= kLeaf) {
         em.leaves(ws, o, n);
         return;
     }
     const int n1 = kTile * ((n + 2 * kTile - 1) / (2 * kTile));
     const int n2 = n - n1;
-    inverse_rec(ws, o, n1, em);
+    inverse_rec(ws, o, n1, em, depth + 1);
 
     std::vector<SliceReq> sl;
     std::vector<GemmSpec> g;
@@ -491,6 +575,30 @@ void inverse_rec(const std::vector<InvWs>& ws, int o, int n, Emitter& em) {
     }
     em.slices(sl);
     em.gemms(g);
+    // ---- side branch: T^T = (L21 X11)^T (B operand rows = XT11, upper
+    // block-triangular) only needs L21 and X11, so it runs concurrently with
+    // the trailing update and the recursion on A22; depth-private buffers
+    em.side_begin(depth);
+    sl.clear();
+    g.clear();
+    for (const InvWs& w : ws) {
+        sl.push_back(slice_of(w.l, w.ld, o + n1, o, n2, n1, w.side0[depth], SLICE_FULL));
+        sl.push_back(slice_of(w.xt, w.ld, o, o, n1, n1, w.side1[depth], SLICE_UPPER_BLOCK));
+        GemmSpec s;
+        s.a = sliced_view(w.side0[depth], n2, n1);
+        s.b = sliced_view(w.side1[depth], n1, n1);
+        s.rows = n2;
+        s.cols = n1;
+        s.k = n1;
+        s.k_mode = K_FROM_COL_TILE;
+        s.flags = EPI_TRANSPOSE;
+        s.c = at(w.t, w.ld, w.t_row[depth], 0);  // T^T [n1 x n2]
+        s.ldc = w.ld;
+        g.push_back(s);
+    }
+    em.slices(sl);
+    em.gemms(g);
+    em.side_end(depth);
     // ---- A22 -= L21 L21^T
     sl.clear();
     g.clear();
@@ -512,34 +620,15 @@ void inverse_rec(const std::vector<InvWs>& ws, int o, int n, Emitter& em) {
     em.slices(sl);
     em.gemms(g);
 
-    inverse_rec(ws, o + n1, n2, em);
+    inverse_rec(ws, o + n1, n2, em, depth + 1);
 
-    // ---- T^T = (L21 X11)^T : B operand rows = XT11 (upper block-triangular)
-    sl.clear();
-    g.clear();
-    for (const InvWs& w : ws) {
-        sl.push_back(slice_of(w.l, w.ld, o + n1, o, n2, n1, w.s0, SLICE_FULL));
-        sl.push_back(slice_of(w.xt, w.ld, o, o, n1, n1, w.s1, SLICE_UPPER_BLOCK));
-        GemmSpec s;
-        s.a = sliced_view(w.s0, n2, n1);
-        s.b = sliced_view(w.s1, n1, n1);
-        s.rows = n2;
-        s.cols = n1;
-        s.k = n1;
-        s.k_mode = K_FROM_COL_TILE;
-        s.flags = EPI_TRANSPOSE;
-        s.c = w.t;  // T^T [n1 x n2], ld = w.ld
-        s.ldc = w.ld;
-        g.push_back(s);
-    }
-    em.slices(sl);
-    em.gemms(g);
     // ---- X21 = -X22 T  (B operand rows = T^T), also stored as XT12
+    em.side_join(depth);
     sl.clear();
     g.clear();
     for (const InvWs& w : ws) {
         sl.push_back(slice_of(w.x, w.ld, o + n1, o + n1, n2, n2, w.s0, SLICE_LOWER_BLOCK));
-        sl.push_back(slice_of(w.t, w.ld, 0, 0, n1, n2, w.s1, SLICE_FULL));
+        sl.push_back(slice_of(w.t, w.ld, w.t_row[depth], 0, n1, n2, w.s1, SLICE_FULL));
         GemmSpec s;
         s.a = sliced_view(w.s0, n2, n2);
         s.b = sliced_view(w.s1, n1, n2);
@@ -1017,7 +1106,7 @@ int pf_damped_inverse_batched(const pf_inverse_problem* problems, int count, voi
             run_program(groups, st);  // one persistent launch for every group
         } else {
             run_forked(groups.size(), st, [&](std::size_t g, cudaStream_t s) {
-                StreamEmitter em(s);
+                StreamEmitter em(s, static_cast<int>(g));
                 damped_inverse_group(groups[g], em);
             });
         }
