@@ -480,6 +480,7 @@ def pipeline_section(args, rank, world, local_rank, dist):
     cfg = S.PipelineConfig(method=method, stages=spec["stages"], micro_batches=spec["micro_batches"],
                            micro_batch_size=32, replicas=spec["replicas"], layers_per_stage=L, seq_len=128)
     costs_box = {"costs": "measured"}  # profiler -> CostTable closed loop (engine.measure_stage_times)
+    t_meas = {}
     out = {"model": "BERT-Large (24 x 1024, FFN 4096, 16 heads), random init", "method": spec["method"],
            "stages": cfg.stages, "micro_batches": cfg.micro_batches, "micro_batch": "32 x 128",
            "replicas": cfg.replicas, "layers_per_stage": L, "data": "synthetic token ids, 15% MLM"}
@@ -489,6 +490,7 @@ def pipeline_section(args, rank, world, local_rank, dist):
                               refresh=2, costs=costs_box["costs"], dist=dist, seed=11)
         if t.measured is not None:
             m = t.measured
+            t_meas["times"] = m
             costs_box["costs"] = t.costs
             costs_box["measured"] = {"t_f_ms": m.f, "t_b_ms": m.b, "curvature_item_ms": m.curv,
                                      "inversion_item_ms": m.inv, "precondition_stage_ms": m.prec,
@@ -523,6 +525,21 @@ def pipeline_section(args, rank, world, local_rank, dist):
                     "util_definition": "union of F/B/K-FAC/collective op intervals (CUDA events) / cycle wall time, min over ranks"})
         if "measured" in costs_box:
             out["measured_costs"] = costs_box["measured"]
+        if world == 1 and t_meas.get("times") is not None:
+            # BASELINE configs 2-4 on 2/4/8 B200, SIMULATED by the reference
+            # assigner from the item costs measured here (the driver's tiers run
+            # one GPU); the 8-GPU row is the north-star Chimera config
+            from paper_2211_14133_b200.engine import project_pipeline
+            proj = {}
+            for n_gpu, sp in sorted(PIPELINE_LADDER.items()):
+                if n_gpu == 1:
+                    continue
+                m = S.parse_method(sp["method"])
+                pc = S.PipelineConfig(method=m, stages=sp["stages"], micro_batches=sp["micro_batches"],
+                                      micro_batch_size=32, replicas=sp["replicas"],
+                                      layers_per_stage=bert.layers // sp["stages"], seq_len=128)
+                proj[f"{n_gpu}gpu_{sp['method']}_D{sp['stages']}"] = project_pipeline(t_meas["times"], pc)
+            out["projected_from_measured_costs"] = proj
     except Exception as e:  # reported, never fatal for the bench line
         out["error"] = f"{type(e).__name__}: {e}"[:400]
     return out

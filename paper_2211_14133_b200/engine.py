@@ -325,6 +325,34 @@ def costs_from_times(t: MeasuredTimes, comm_alpha_ms: float = 0.01,
                        m_curv=t.factor_bytes, comm_alpha=comm_alpha_ms, comm_beta=comm_bytes_per_ms)
 
 
+def project_pipeline(t: MeasuredTimes, cfg: S.PipelineConfig) -> dict:
+    """Simulate `cfg` with the reference assigner from per-LAYER item costs
+    measured on this GPU (one stage of t.layers layers): F/B and precondition
+    scale with the layers per stage, curvature / inversion items are per layer
+    already.  Returns the plain pipeline period (F/B only), the PipeFisher
+    period (refresh cycle / refresh steps, K-FAC items in bubbles + tail), the
+    refresh period and the simulated utilisation.  A projection, not a
+    measurement."""
+    spd = 2 if cfg.method == S.Method.Chimera else 1
+    l = cfg.layers_per_stage
+    per = lambda v: v / t.layers * l  # noqa: E731
+    costs = costs_from_times(MeasuredTimes(f=per(t.f), b=per(t.b), curv=t.curv, inv=t.inv, prec=per(t.prec),
+                                           layers=l, stages_per_device=spd,
+                                           param_bytes=int(per(t.param_bytes)),
+                                           factor_bytes=int(per(t.factor_bytes))))
+    base = S.build_schedule(cfg, costs)
+    plain_ms = S.schedule_metrics(base)[0]
+    try:
+        filled = S.assign_works(base, cfg, costs, S.enumerate_kfac_works(cfg, costs), S.AssignOptions())
+    except S.InfeasibleError as e:
+        return {"plain_step_ms": plain_ms, "infeasible": str(e)[:200]}
+    span, util, _ = S.schedule_metrics(filled.schedule)
+    period = span / filled.refresh_period
+    return {"plain_step_ms": plain_ms, "pipefisher_step_ms": period, "step_ratio_vs_plain": period / plain_ms,
+            "refresh_period": filled.refresh_period, "simulated_util": util,
+            "cost_table": {k: getattr(costs, k) for k in ("t_f", "t_b", "t_curv", "t_inv", "t_prec")}}
+
+
 def measure_stage_times(backend: "CudaBackend", reps: int = 3) -> MeasuredTimes:
     """Time the work items of this rank's first hosted stage.  Mutates the
     backend's model and K-FAC state: use a throw-away backend."""

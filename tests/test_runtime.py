@@ -232,3 +232,17 @@ def test_measured_costs_follow_reference_semantics():
     base = S.build_schedule(cfg, c)
     filled = S.assign_works(base, cfg, c, q, S.AssignOptions())
     assert filled.refresh_period >= 1
+
+
+def test_pipeline_projection_from_measured_costs():
+    """engine.project_pipeline: per-layer item costs -> the reference assigner
+    on a D-stage config; PipeFisher period >= plain period, refresh >= 1."""
+    from paper_2211_14133_b200.engine import MeasuredTimes, project_pipeline
+    t = MeasuredTimes(f=12.0, b=24.0, curv=0.1, inv=1.0, prec=2.4, layers=24, stages_per_device=1,
+                      param_bytes=10 ** 9, factor_bytes=10 ** 9)
+    cfg = S.PipelineConfig(method=S.Method.GPipe, stages=4, micro_batches=4, micro_batch_size=32,
+                           replicas=1, layers_per_stage=6, seq_len=128)
+    r = project_pipeline(t, cfg)
+    assert r["cost_table"]["t_f"] == 3.0 and r["cost_table"]["t_inv"] == 6.0
+    assert r["pipefisher_step_ms"] >= r["plain_step_ms"] and r["refresh_period"] >= 1
+    assert 0.0 < r["simulated_util"] <= 1.0
