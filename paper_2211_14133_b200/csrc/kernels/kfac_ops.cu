@@ -155,6 +155,16 @@ Sliced sliced_view(void* base, int rows, int k) {
     return s;
 }
 
+// rows [r0, r0 + n) of a sliced operand (same planes, 16-byte aligned offset)
+Sliced rows_of(const Sliced& s, int r0, int n) {
+    Sliced t = s;
+    t.planes = s.planes + static_cast<int64_t>(r0) * s.kpad;
+    t.rows = n;
+    t.exps = s.exps + r0;
+    t.sqnorm = s.sqnorm + r0;
+    return t;
+}
+
 struct SliceReq {
     const float* src;
     int ld;
@@ -546,14 +556,22 @@ SliceReq slice_of(float* src, int ld, int r0, int c0, int rows, int k, void* slo
 //   recurse on A22
 //   T^T  = (L21 X11)^T          (via XT11)
 //   X21  = -X22 T,  XT12 = X21^T
-void inverse_rec(const std::vector<InvWs>& ws, int o, int n, Emitter& em, int depth = 0) {
+// `pending`: depth of an ancestor side branch that still updates this node's
+// A21 / A22 (the parent's look-ahead), joined before this node's first GEMM.
+void inverse_rec(const std::vector<InvWs>& ws, int o, int n, Emitter& em, int depth = 0, int pending = -1) {
     if (n <= kLeaf) {
         em.leaves(ws, o, n);
         return;
     }
     const int n1 = kTile * ((n + 2 * kTile - 1) / (2 * kTile));
     const int n2 = n - n1;
+    // look-ahead: when A22 is itself an internal node, only its top-left
+    // n1' x n1' block must be updated before the recursion descends into it;
+    // the rest of the trailing update joins the side branch
+    const int n1c = kTile * ((n2 + 2 * kTile - 1) / (2 * kTile));
+    const bool split = n2 > kLeaf;
     inverse_rec(ws, o, n1, em, depth + 1);
+    if (pending >= 0) em.side_join(pending);
 
     std::vector<SliceReq> sl;
     std::vector<GemmSpec> g;
@@ -596,18 +614,48 @@ void inverse_rec(const std::vector<InvWs>& ws, int o, int n, Emitter& em, int de
         s.ldc = w.ld;
         g.push_back(s);
     }
+    if (split) {  // the rest of A22 -= L21 L21^T (rows n1c .. n2), from the side's L21 digits
+        for (const InvWs& w : ws) {
+            const Sliced l21 = sliced_view(w.side0[depth], n2, n1);
+            GemmSpec a;  // A22[n1c:, :n1c] -= L21[n1c:] L21[:n1c]^T
+            a.a = rows_of(l21, n1c, n2 - n1c);
+            a.b = rows_of(l21, 0, n1c);
+            a.rows = n2 - n1c;
+            a.cols = n1c;
+            a.k = n1;
+            a.alpha = -1.0f;
+            a.beta = 1.0f;
+            a.flags = EPI_VEC4;
+            a.c = at(w.a, w.ld, o + n1 + n1c, o + n1);
+            a.ldc = w.ld;
+            g.push_back(a);
+            GemmSpec b;  // A22[n1c:, n1c:] -= L21[n1c:] L21[n1c:]^T  (lower)
+            b.a = rows_of(l21, n1c, n2 - n1c);
+            b.b = b.a;
+            b.rows = b.cols = n2 - n1c;
+            b.k = n1;
+            b.lower = true;
+            b.alpha = -1.0f;
+            b.beta = 1.0f;
+            b.flags = EPI_VEC4;
+            b.c = at(w.a, w.ld, o + n1 + n1c, o + n1 + n1c);
+            b.ldc = w.ld;
+            g.push_back(b);
+        }
+    }
     em.slices(sl);
     em.gemms(g);
     em.side_end(depth);
-    // ---- A22 -= L21 L21^T
+    // ---- A22 -= L21 L21^T  (look-ahead: only the top-left n1c x n1c block here)
     sl.clear();
     g.clear();
+    const int nu = split ? n1c : n2;
     for (const InvWs& w : ws) {
-        sl.push_back(slice_of(w.l, w.ld, o + n1, o, n2, n1, w.s0, SLICE_FULL));
+        sl.push_back(slice_of(w.l, w.ld, o + n1, o, nu, n1, w.s0, SLICE_FULL));
         GemmSpec s;
-        s.a = sliced_view(w.s0, n2, n1);
+        s.a = sliced_view(w.s0, nu, n1);
         s.b = s.a;
-        s.rows = s.cols = n2;
+        s.rows = s.cols = nu;
         s.k = n1;
         s.lower = true;
         s.alpha = -1.0f;
@@ -620,7 +668,7 @@ void inverse_rec(const std::vector<InvWs>& ws, int o, int n, Emitter& em, int de
     em.slices(sl);
     em.gemms(g);
 
-    inverse_rec(ws, o + n1, n2, em, depth + 1);
+    inverse_rec(ws, o + n1, n2, em, depth + 1, split ? depth : -1);
 
     // ---- X21 = -X22 T  (B operand rows = T^T), also stored as XT12
     em.side_join(depth);
