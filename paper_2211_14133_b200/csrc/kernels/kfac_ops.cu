@@ -291,20 +291,35 @@ struct DampBatch {
     Damp2D e[kMaxDamp];
 };
 
-// dst = M + damping * I  (lower triangle incl. diagonal; the rest never read)
-__global__ void damp_kernel(const __grid_constant__ DampBatch b) {
+// dst = M + damping * I, lower triangle incl. diagonal (the rest is never
+// read; whole float4 groups are copied).  One warp per row, 8 rows per CTA.
+__global__ void __launch_bounds__(256) damp_kernel(const __grid_constant__ DampBatch b) {
     const Damp2D& s = b.e[blockIdx.y];
     ptx::grid_dep_wait();
     ptx::grid_dep_launch();
     if (blockIdx.x == 0 && threadIdx.x == 0) *s.info = 0;
-    const int64_t total = static_cast<int64_t>(s.d) * s.d;
-    for (int64_t idx = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; idx < total;
-         idx += static_cast<int64_t>(gridDim.x) * blockDim.x) {
-        const int r = static_cast<int>(idx / s.d), c = static_cast<int>(idx % s.d);
-        if (c > r) continue;
-        float v = s.src[static_cast<int64_t>(r) * s.ld_src + c];
-        if (r == c) v += s.damping;
-        s.dst[static_cast<int64_t>(r) * s.ld_dst + c] = v;
+    const int r = blockIdx.x * 8 + static_cast<int>(threadIdx.x >> 5);
+    const int lane = threadIdx.x & 31;
+    if (r >= s.d) return;
+    const float* src = s.src + static_cast<int64_t>(r) * s.ld_src;
+    float* dst = s.dst + static_cast<int64_t>(r) * s.ld_dst;
+    const bool vec = (s.ld_src % 4 == 0) && (s.ld_dst % 4 == 0) && ((reinterpret_cast<uintptr_t>(s.src) & 15) == 0) &&
+                     ((reinterpret_cast<uintptr_t>(s.dst) & 15) == 0);
+    if (vec) {
+        const int n4 = (r + 4) / 4;  // float4 groups covering columns [0, r]
+        for (int c4 = lane; c4 < n4; c4 += 32) {
+            float4 v = __ldcg(reinterpret_cast<const float4*>(src) + c4);
+            if (c4 == r / 4) {
+                const int e = r % 4;
+                if (e == 0) v.x += s.damping;
+                if (e == 1) v.y += s.damping;
+                if (e == 2) v.z += s.damping;
+                if (e == 3) v.w += s.damping;
+            }
+            reinterpret_cast<float4*>(dst)[c4] = v;
+        }
+    } else {
+        for (int c = lane; c <= r; c += 32) dst[c] = __ldcg(src + c) + (c == r ? s.damping : 0.0f);
     }
 }
 
@@ -464,8 +479,7 @@ struct StreamEmitter final : Emitter {
             db.e[i] = jobs[i];
             d = std::max(d, jobs[i].d);
         }
-        const int blocks = std::min((d * d + 255) / 256, 148 * 8);
-        launch(damp_kernel, dim3(blocks, static_cast<unsigned>(jobs.size())), dim3(256), 0, st, db);
+        launch(damp_kernel, dim3((d + 7) / 8, static_cast<unsigned>(jobs.size())), dim3(256), 0, st, db);
         after_launch("damp_kernel");
     }
     void slices(const std::vector<SliceReq>& reqs) override { launch_slices(reqs, st); }
