@@ -129,12 +129,7 @@ __device__ __noinline__ void graph_gemm_tile(const GraphProgram& g, int di, int 
     using T = GOZ;
     const GemmDesc P = g.gemms[di];  // by value: stores below must not force reloads
     int tm, tn;
-    if (P.lower) {
-        decode_lower(lt, tm, tn);
-    } else {
-        tm = lt / P.tiles_n;
-        tn = lt % P.tiles_n;
-    }
+    map_tile(P, lt, tm, tn);
     int k_begin = 0, k_end = P.k;
     if (P.k_mode == K_FROM_ROW_TILE) k_begin = tm * kTile;
     if (P.k_mode == K_FROM_COL_TILE) k_begin = tn * kTile;

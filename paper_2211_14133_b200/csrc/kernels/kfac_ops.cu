@@ -276,6 +276,14 @@ void launch_gemms(const std::vector<GemmSpec>& specs, cudaStream_t stream) {
         }
         batch.n_probs = probs;
         batch.total_tiles = tiles;
+        batch.interleave = probs > 1 ? 1 : 0;
+        for (int q = 1; q < probs; ++q) {
+            const GemmDesc& a = batch.probs[0];
+            const GemmDesc& b = batch.probs[q];
+            if (desc_tiles(a) != desc_tiles(b) || a.k_mode != b.k_mode || a.lower != b.lower ||
+                a.tiles_m != b.tiles_m || a.tiles_n != b.tiles_n || a.k != b.k)
+                batch.interleave = 0;
+        }
         if (tiles == 0) continue;
         launch(kernel, dim3(tiles), dim3(T::kThreads), T::kSmemBytes, stream, batch);
         after_launch("umma_gemm_kernel");

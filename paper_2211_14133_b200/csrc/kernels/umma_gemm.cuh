@@ -91,6 +91,7 @@ struct GemmBatch {
     GemmDesc probs[kMaxProbs];
     int n_probs;
     int total_tiles;
+    int interleave;  // all problems share tile count and k-mode: tile rank major, problem minor
 };
 
 template <int kFmt>
@@ -112,6 +113,34 @@ struct GemmTraits {
         kFmt == kOZ8 ? ((2u << 4) | (1u << 7) | (1u << 10) | ((128u >> 3) << 17) | ((128u >> 4) << 24))
                      : ptx::make_idesc(1, 128, 128);
 };
+
+__device__ __forceinline__ void decode_lower(int t, int& tm, int& tn);
+
+// Local tile index -> (tm, tn), longest k-range first (LPT): with triangular
+// k-ranges the last wave would otherwise wait on the longest tiles.
+__device__ __forceinline__ void map_tile(const GemmDesc& P, int lt, int& tm, int& tn) {
+    if (P.lower) {  // decode_lower walks tm ascending: K_FROM_ROW_TILE longest first
+        decode_lower(lt, tm, tn);
+        return;
+    }
+    switch (P.k_mode) {
+        case K_TO_COL_TILE_END:  // k-length grows with tn
+            tn = P.tiles_n - 1 - lt / P.tiles_m;
+            tm = lt % P.tiles_m;
+            break;
+        case K_FROM_COL_TILE:  // shrinks with tn
+            tn = lt / P.tiles_m;
+            tm = lt % P.tiles_m;
+            break;
+        case K_TO_ROW_TILE_END:  // grows with tm
+            tm = P.tiles_m - 1 - lt / P.tiles_n;
+            tn = lt % P.tiles_n;
+            break;
+        default:
+            tm = lt / P.tiles_n;
+            tn = lt % P.tiles_n;
+    }
+}
 
 __device__ __forceinline__ void decode_lower(int t, int& tm, int& tn) {
     int m = static_cast<int>((sqrtf(8.0f * static_cast<float>(t) + 1.0f) - 1.0f) * 0.5f);
@@ -253,17 +282,17 @@ __global__ void __launch_bounds__(GemmTraits<kFmt>::kThreads, GemmTraits<kFmt>::
     float* col_scale = reinterpret_cast<float*>(smem + kStages * T::kStageBytes + 256);  // kOZ8: 2^e_b per tile column
 
     const int gt = blockIdx.x;
-    int p = 0;
-    while (p + 1 < batch.n_probs && batch.probs[p + 1].tile_begin <= gt) ++p;
-    const GemmDesc& P = batch.probs[p];
-    const int lt = gt - P.tile_begin;
-    int tm, tn;
-    if (P.lower) {
-        decode_lower(lt, tm, tn);
+    int p = 0, lt;
+    if (batch.interleave) {
+        p = gt % batch.n_probs;
+        lt = gt / batch.n_probs;
     } else {
-        tm = lt / P.tiles_n;
-        tn = lt % P.tiles_n;
+        while (p + 1 < batch.n_probs && batch.probs[p + 1].tile_begin <= gt) ++p;
+        lt = gt - batch.probs[p].tile_begin;
     }
+    const GemmDesc& P = batch.probs[p];
+    int tm, tn;
+    map_tile(P, lt, tm, tn);
     int k_begin = 0, k_end = P.k;
     if (P.k_mode == K_FROM_ROW_TILE) k_begin = tm * kTile;
     if (P.k_mode == K_FROM_COL_TILE) k_begin = tn * kTile;
