@@ -299,3 +299,22 @@ def ref_assign_dump(cfg, costs, inversion_parallel=False, horizon_cap=10) -> Dum
     c, t = _structs(cfg, costs)
     return _parse(_call_dump(ref().pfref_assign_dump, C.byref(c), C.byref(t),
                              int(inversion_parallel), horizon_cap))
+
+
+def ref_assign_trace(cfg, costs, inversion_parallel=False, horizon_cap=10, devices_per_group=0) -> str:
+    """io::trace_to_json (proj/src/io/trace.cpp:38-63) of the reference's
+    assign_works schedule (oracle/_ref built with nlohmann json)."""
+    c, t = _structs(cfg, costs)
+    return _call_dump(ref().pfref_assign_trace, C.byref(c), C.byref(t), int(inversion_parallel), horizon_cap,
+                      devices_per_group)
+
+
+def ref_block_diag_split(m: np.ndarray, k: int):
+    """kfac::block_diag_split_factor + inversion_flops (proj/src/kfac/kfac.cpp:203-226)."""
+    m = np.ascontiguousarray(m, dtype=np.float64)
+    d = m.shape[0]
+    b = d // k
+    out = np.zeros((k, b, b))
+    ff, fb = C.c_double(), C.c_double()
+    _ref_call(ref().pfref_block_diag_split(_ptr(m), d, k, _ptr(out), C.byref(ff), C.byref(fb)))
+    return list(out), ff.value, fb.value

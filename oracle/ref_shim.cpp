@@ -19,6 +19,9 @@
 #include <vector>
 
 #include "pipefill/bubblefill.hpp"
+#ifdef PFREF_TRACE
+#include "pipefill/io/trace.hpp"
+#endif
 #include "pipefill/kfac/kfac.hpp"
 #include "pipefill/kfac/matrix.hpp"
 #include "pipefill/schedule.hpp"
@@ -193,6 +196,37 @@ int pfref_assign_dump(const RefConfig* c, const RefCosts* t, int inversion_paral
             for (const auto& w : e.unplaced) dump_work(out, "U", w);
         }
         return emit(out, buf, cap, need);
+    });
+}
+
+#ifdef PFREF_TRACE
+// io::trace_to_json (trace.hpp:15) of the assign_works schedule of the config.
+int pfref_assign_trace(const RefConfig* c, const RefCosts* t, int inversion_parallel, int horizon_cap,
+                       int devices_per_group, char* buf, size_t cap, size_t* need) {
+    return shield([&] {
+        const auto cfg = cfg_of(c);
+        const auto costs = costs_of(t);
+        const auto base = build_schedule(cfg, costs, 1);
+        const auto queue = enumerate_kfac_works(cfg, costs);
+        AssignOptions o;
+        o.inversion_parallel = inversion_parallel != 0;
+        o.horizon_cap = horizon_cap;
+        const auto f = assign_works(base, cfg, costs, queue, o);
+        return emit(io::trace_to_json(f.schedule, devices_per_group), buf, cap, need);
+    });
+}
+#endif
+
+// kfac::block_diag_split_factor + inversion flops (kfac.cpp:203-226).
+int pfref_block_diag_split(const double* m, int d, int k, double* out_blocks, double* flops_full,
+                           double* flops_blocks) {
+    return shield([&] {
+        const auto parts = kfac::block_diag_split_factor(mat(m, d, d), k);
+        const int b = d / k;
+        for (int i = 0; i < k; ++i) unmat(parts[static_cast<size_t>(i)], out_blocks + static_cast<size_t>(i) * b * b);
+        *flops_full = kfac::inversion_flops(d);
+        *flops_blocks = kfac::block_diag_inversion_flops(d, k);
+        return 0;
     });
 }
 

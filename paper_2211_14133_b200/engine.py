@@ -12,6 +12,7 @@ Per hosted stage and encoder layer the factor sets are:
 """
 from __future__ import annotations
 
+import math
 import time
 from dataclasses import dataclass
 from typing import Dict, List, Optional, Tuple
@@ -91,8 +92,9 @@ class CudaBackend:
                      for m in range(cfg.micro_batches)}
         self.saved: Dict[Tuple[int, int], Tuple] = {}
         self.losses: List[torch.Tensor] = []
-        self.timeline: List[Tuple[str, torch.cuda.Event, torch.cuda.Event]] = []
+        self.timeline: List[Tuple[str, torch.cuda.Event, torch.cuda.Event, dict]] = []
         self.record = False
+        self.cur_step = 0  # set by the executor before each op (trace metadata)
 
     # ------------------------------------------------------------ timing helpers
     def _begin(self, stream):
@@ -102,12 +104,13 @@ class CudaBackend:
         e.record(stream)
         return e
 
-    def _end(self, kind, e0, stream):
+    def _end(self, kind, e0, stream, **meta):
         if e0 is None:
             return
         e1 = torch.cuda.Event(enable_timing=True)
         e1.record(stream)
-        self.timeline.append((kind, e0, e1))
+        meta.setdefault("step", self.cur_step)
+        self.timeline.append((kind, e0, e1, meta))
 
     def mark_compute(self):
         ev = torch.cuda.Event()
@@ -130,7 +133,7 @@ class CudaBackend:
         out = mod(inp, pos, labels)
         mod.store.active_micro = None
         self.saved[(stage, micro)] = (inp, out)
-        self._end("F", e0, self.compute)
+        self._end("F", e0, self.compute, stage=stage, micro_batch=micro)
         if mod.is_last:
             self.losses.append(out.detach())
             return None
@@ -146,7 +149,7 @@ class CudaBackend:
         else:
             out.backward(gy.to(out.dtype))
         mod.store.active_micro = None
-        self._end("B", e0, self.compute)
+        self._end("B", e0, self.compute, stage=stage, micro_batch=micro)
         return None if mod.is_first else inp.grad.to(torch.bfloat16)
 
     # ------------------------------------------------------------ K-FAC items
@@ -178,7 +181,8 @@ class CudaBackend:
                 ks.started[(layer, f)] = True
             if probs:
                 K.syrk(probs, fill_upper=False)
-            self._end("CURV", e0, self.kfac_stream)
+            st0, l0, f0, m0 = items[0]
+            self._end("CURV", e0, self.kfac_stream, stage=st0, layer=l0, factor=f0, micro_batch=m0, items=len(items))
 
     def sync_curvature(self, stage, layer, f, group, gate):
         ks = self.kstate[stage]
@@ -190,7 +194,7 @@ class CudaBackend:
                 import torch.distributed as dist
                 for key in ks.keys(f):
                     dist.all_reduce(ks.factor[(layer, key)], op=dist.ReduceOp.AVG, group=group)
-            self._end("SYNC_CURV", e0, self.kfac_stream)
+            self._end("SYNC_CURV", e0, self.kfac_stream, stage=stage, layer=layer, factor=f)
 
     def invert(self, stage, layer, f, gate):
         self.invert_many([(stage, layer, f)], gate)
@@ -216,7 +220,8 @@ class CudaBackend:
                     digs.append(o.digits)
             e0 = self._begin(self.kfac_stream)
             K.damped_inverse_batched(mats, self.damping, outs, digs, check=False)
-            self._end("INV", e0, self.kfac_stream)
+            st0, l0, f0 = items[0]
+            self._end("INV", e0, self.kfac_stream, stage=st0, layer=l0, factor=f0, items=len(items))
             ev = torch.cuda.Event()
             ev.record(self.kfac_stream)
         for stage, layer, f in items:
@@ -254,7 +259,7 @@ class CudaBackend:
         for g in grads:
             g.copy_(flat[off:off + g.numel()].view_as(g))
             off += g.numel()
-        self._end("SYNC_GRAD", e0, self.compute)
+        self._end("SYNC_GRAD", e0, self.compute, stage=stage)
 
     def precondition(self, stage, step):
         mod = self.stages[stage]
@@ -290,7 +295,7 @@ class CudaBackend:
                 if p.grad is not None and id(p) not in kfac_params:
                     p.add_(p.grad, alpha=-self.lr)
                 p.grad = None
-        self._end("PREC", e0, self.compute)
+        self._end("PREC", e0, self.compute, stage=stage, step=step)
 
     def end_cycle(self):
         for mod in self.stages.values():
@@ -503,7 +508,9 @@ class PipeFisherTrainer:
         cycle_ms = t0.elapsed_time(t1)
         busy = 0.0
         if record and b.timeline:
-            iv = sorted((t0.elapsed_time(e0), t0.elapsed_time(e1)) for _, e0, e1 in b.timeline)
+            iv = sorted((t0.elapsed_time(e0), t0.elapsed_time(e1)) for _, e0, e1, _ in b.timeline)
+            self.last_trace = [(k, t0.elapsed_time(e0), t0.elapsed_time(e1), m) for k, e0, e1, m in b.timeline]
+            self.last_cycle_ms = cycle_ms
             cur_b, cur_e = iv[0]
             for s, e in iv[1:]:
                 if s > cur_e:
@@ -515,6 +522,70 @@ class PipeFisherTrainer:
         loss = float(torch.stack(b.losses).mean()) if b.losses else None
         return CycleResult(cycle_ms, cycle_ms / self.refresh, busy / cycle_ms if cycle_ms > 0 else 0.0,
                            busy, loss)
+
+
+_TRACE_KIND = {"F": S.WorkKind.Forward, "B": S.WorkKind.Backward, "CURV": S.WorkKind.Curvature,
+               "INV": S.WorkKind.Inversion, "PREC": S.WorkKind.Precondition, "SYNC_GRAD": S.WorkKind.SyncGrad,
+               "SYNC_CURV": S.WorkKind.SyncCurvature}
+
+
+def _trace_event(kind, start_ms, dur_ms, device, devices_per_group, stage, step, micro=None, layer=None,
+                 factor=None, extra=None):
+    """One event of the reference trace schema (proj/src/io/trace.cpp:38-63):
+    Chrome 'X' events, ts/dur in us, pid = replica group, tid = device, name
+    'kind [lL] [A|B] [mM]' or 'kind sS'."""
+    name = S.kind_name(kind)
+    if layer is not None:
+        name += f" l{layer}"
+    if factor is not None:
+        name += " " + ("A" if int(factor) == 0 else "B")
+    if micro is not None:
+        name += f" m{micro}"
+    if layer is None and factor is None and micro is None:
+        name += f" s{stage}"
+    args = {"kind": S.kind_name(kind), "stage": stage, "step": step}
+    if micro is not None:
+        args["micro_batch"] = micro
+    if layer is not None:
+        args["layer"] = layer
+    if factor is not None:
+        args["factor"] = "A" if int(factor) == 0 else "B"
+    if extra:
+        args.update(extra)
+    def llround(v):  # std::llround: halves away from zero
+        return int(math.floor(abs(v) + 0.5)) * (1 if v >= 0 else -1)
+
+    return {"name": name, "ph": "X", "ts": llround(start_ms * 1000.0), "dur": llround(dur_ms * 1000.0),
+            "pid": device // devices_per_group if devices_per_group > 0 else 0, "tid": device, "args": args}
+
+
+def schedule_trace(schedule: S.StaticSchedule, devices_per_group: int = 0) -> dict:
+    """The reference's trace_to_json for a (simulated) schedule."""
+    ev = []
+    for d, line in enumerate(schedule.timelines):
+        for it in line:
+            ev.append(_trace_event(it.kind, it.start, it.duration, d, devices_per_group, it.stage, it.step,
+                                   it.micro_batch, it.layer, it.factor))
+    return {"traceEvents": ev}
+
+
+def measured_trace(trainer: "PipeFisherTrainer") -> dict:
+    """The last recorded cycle (run_cycle(record=True)) of this rank as MEASURED
+    intervals (CUDA events on the launching streams) in the same schema, plus
+    utilisation by the reference definition (schedule.cpp:257-270: sum of item
+    durations / (makespan x devices)) and by the union of busy intervals (the
+    K-FAC stream overlaps the compute stream, so the sum can exceed the span)."""
+    ev, busy_sum = [], 0.0
+    for kind, a, b, m in getattr(trainer, "last_trace", []):
+        extra = {"items": m["items"]} if "items" in m else None
+        ev.append(_trace_event(_TRACE_KIND[kind], a, b - a, trainer.rank, trainer.topo.D, m.get("stage", -1),
+                               m.get("step", 0), m.get("micro_batch"), m.get("layer"), m.get("factor"), extra))
+        busy_sum += b - a
+    span = getattr(trainer, "last_cycle_ms", 0.0)
+    return {"traceEvents": ev,
+            "otherData": {"source": "measured: CUDA events around each op on its stream (batched items = one event)",
+                          "cycle_ms": span, "refresh_steps": trainer.refresh,
+                          "util_reference_definition": busy_sum / span if span > 0 else 0.0}}
 
 
 class _LocalComm:

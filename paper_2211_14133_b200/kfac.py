@@ -195,6 +195,59 @@ def damped_inverse_batched(mats: Sequence[torch.Tensor], damping: float,
     return outs
 
 
+def block_diag_split_factor(m: torch.Tensor, k: int) -> List[torch.Tensor]:
+    """kfac.cpp:203-218: the K diagonal blocks of a square factor (copies)."""
+    if m.dim() != 2 or m.shape[0] != m.shape[1]:
+        raise ValueError("factor must be square")
+    d = m.shape[0]
+    if k < 1 or d % k != 0:
+        raise ValueError("K must divide the factor dimension")
+    b = d // k
+    return [m[i * b:(i + 1) * b, i * b:(i + 1) * b].clone() for i in range(k)]
+
+
+def inversion_flops(dim: int) -> float:
+    """kfac.cpp:220-222 (the reference cost model's (2/3) d^3)."""
+    return (2.0 / 3.0) * float(dim) * dim * dim
+
+
+def block_diag_inversion_flops(dim: int, k: int) -> float:
+    """kfac.cpp:224-227."""
+    if k < 1 or dim % k != 0:
+        raise ValueError("K must divide the dimension")
+    return k * inversion_flops(dim // k)
+
+
+def damped_inverse_block_diag(mats: Sequence[torch.Tensor], damping: float, k: int,
+                              outs: Optional[Sequence[torch.Tensor]] = None,
+                              digits: Optional[Sequence[torch.Tensor]] = None,
+                              check: bool = True) -> List[torch.Tensor]:
+    """Block-diagonal K-FAC for large factors (§A, kfac.cpp:203-226):
+    each factor is replaced by its K diagonal blocks, so its inversion costs
+    d^3 / K^2.  The damped inverses of every block of every factor run as ONE
+    batched call, reading and writing views of the full matrices (no copies);
+    the off-diagonal blocks of the inverse are zero.  With ``digits`` the digit
+    form of the assembled block-diagonal inverse is written for the
+    preconditioner."""
+    outs = list(outs) if outs is not None else [torch.empty_like(m, dtype=torch.float32) for m in mats]
+    blocks_in, blocks_out = [], []
+    for m, o in zip(mats, outs):
+        d = m.shape[0]
+        if k < 1 or d % k != 0:
+            raise ValueError("K must divide the factor dimension")
+        b = d // k
+        o.zero_()
+        for i in range(k):
+            blocks_in.append(m[i * b:(i + 1) * b, i * b:(i + 1) * b])
+            blocks_out.append(o[i * b:(i + 1) * b, i * b:(i + 1) * b])
+    damped_inverse_batched(blocks_in, damping, blocks_out, None, check=check)
+    if digits is not None:
+        for o, dg in zip(outs, digits):
+            L.check(L.lib().pf_slice(o.data_ptr(), o.shape[0], o.shape[1], o.stride(0), dg.data_ptr(),
+                                     _stream()), "slice")
+    return outs
+
+
 def cholesky_spd_inverse(m: torch.Tensor, damping: float) -> torch.Tensor:
     """matrix.hpp:58 — (M + damping I)^-1 via Cholesky (fp32-accurate)."""
     return damped_inverse_batched([m], damping)[0]
@@ -274,7 +327,8 @@ def precondition_update_sliced(items: Sequence[Tuple[Optional[torch.Tensor], tor
 class KfacState:
     """kfac.hpp:60-73: per-layer factors, damped inverses (fp32 + digit form), staleness."""
 
-    def __init__(self, layers: int = 0, damping: float = 0.0, learning_rate: float = 0.0):
+    def __init__(self, layers: int = 0, damping: float = 0.0, learning_rate: float = 0.0,
+                 block_diag_k: int = 1):
         self.factor_a: List[Optional[torch.Tensor]] = [None] * layers
         self.factor_b: List[Optional[torch.Tensor]] = [None] * layers
         self.inv_a: List[Optional[SlicedMatrix]] = [None] * layers
@@ -283,6 +337,9 @@ class KfacState:
         self.refreshed_this_step = [False] * layers
         self.damping = damping
         self.learning_rate = learning_rate
+        # > 1: factors whose dimension K divides are inverted block-diagonally
+        # (kfac.cpp:203-226); the others in full
+        self.block_diag_k = block_diag_k
 
     def has_inverses(self, layer: int) -> bool:
         return self.inv_a[layer] is not None and self.inv_b[layer] is not None
@@ -314,7 +371,15 @@ class KfacState:
         outs = [torch.empty_like(m) for m in mats]
         digits = [torch.empty(slice_bytes(m.shape[0], m.shape[0]), dtype=torch.uint8,
                               device=m.device) for m in mats]
-        damped_inverse_batched(mats, self.damping, outs, digits)
+        k = self.block_diag_k
+        bd = [i for i, m in enumerate(mats) if k > 1 and m.shape[0] % k == 0]
+        full = [i for i in range(len(mats)) if i not in set(bd)]
+        if full:
+            damped_inverse_batched([mats[i] for i in full], self.damping, [outs[i] for i in full],
+                                   [digits[i] for i in full])
+        if bd:
+            damped_inverse_block_diag([mats[i] for i in bd], self.damping, k, [outs[i] for i in bd],
+                                      [digits[i] for i in bd])
         for (l, which), o, dg in zip(slots, outs, digits):
             (self.inv_a if which == 0 else self.inv_b)[l] = SlicedMatrix(o, dg)
             self.staleness[l] = 0

@@ -78,6 +78,17 @@ def main():
     with open(os.path.join(HERE, "schedules.json"), "w") as f:
         json.dump(out, f, indent=0, sort_keys=True)
 
+    # io::trace_to_json of assigned schedules (the trace schema the runtime's
+    # measured and simulated timelines are exported in)
+    traces = {}
+    cases = named_cases()
+    for name in ("gpipe_d2n2_hand", "chimera_d4n4_l4_serial", "1f1b_d4n8_recompute"):
+        cfg, costs, inv_par, cap = cases[name]
+        traces[name] = {"devices_per_group": int(cfg.stages),
+                        "trace": json.loads(R.ref_assign_trace(cfg, costs, inv_par, cap, int(cfg.stages)))}
+    with open(os.path.join(HERE, "traces.json"), "w") as f:
+        json.dump(traces, f, indent=0, sort_keys=True)
+
     arrays = {}
     for d_in, d_out, n in ((64, 32, 96), (130, 70, 200)):
         a = R.orc_symmetric(1000 + d_in, (d_in, n), 3 ** 0.5)

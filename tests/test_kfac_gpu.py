@@ -321,3 +321,37 @@ def test_persistent_executor_in_cuda_graph(K, persistent):
     torch.cuda.synchronize()
     for o, w in zip(outs, want):
         assert torch.equal(o, w)
+
+
+@pytest.mark.parametrize("d,k", [(1024, 4), (512, 2), (384, 3)])
+def test_block_diag_inverse_matches_reference_blocks(K, d, k):
+    """Block-diagonal damped inverse (kfac.cpp:203-226): every diagonal block
+    equals the reference cholesky_spd_inverse of the reference's
+    block_diag_split_factor block; the off-diagonal blocks are exactly zero;
+    the digit form reproduces the assembled inverse."""
+    m = spd(500 + d, d)
+    lam = 0.1
+    t = torch.from_numpy(m).float().cuda()
+    dg = torch.empty(K.slice_bytes(d, d), dtype=torch.uint8, device="cuda")
+    (got,) = K.damped_inverse_block_diag([t], lam, k, digits=[dg])
+    got = got.double().cpu().numpy()
+    m32 = m.astype(np.float32).astype(np.float64)
+    blocks, _, _ = R.ref_block_diag_split(m32, k)
+    b = d // k
+    for i, blk in enumerate(blocks):
+        want = R.ref_cholesky_spd_inverse(blk, lam)
+        assert rel_fro(got[i * b:(i + 1) * b, i * b:(i + 1) * b], want) <= 1e-4
+        for j in range(k):
+            if j != i:
+                assert np.all(got[i * b:(i + 1) * b, j * b:(j + 1) * b] == 0.0)
+    assert torch.equal(K.slice_matrix(torch.from_numpy(got).float().cuda()).digits, dg)
+
+
+def test_kfac_state_block_diag_refresh(K):
+    st = K.KfacState(1, damping=0.1, learning_rate=1e-3, block_diag_k=2)
+    st.factor_a[0] = torch.from_numpy(spd(3, 256)).float().cuda()
+    st.factor_b[0] = torch.from_numpy(spd(4, 100)).float().cuda()  # 2 does divide: block-diag too
+    st.refresh_inverses()
+    a = st.inv_a[0].fp32
+    assert torch.all(a[:128, 128:] == 0) and torch.all(a[128:, :128] == 0)
+    assert st.has_inverses(0) and st.staleness[0] == 0

@@ -137,3 +137,19 @@ def test_python_build_oracle_matches_reference(p2p):
             t = S.CostTable(t_f=0.9, t_b=1.7, p2p_latency=p2p)
             lines, _ = O.build_schedule(cfg, t, 2)
             assert H.canonical([it for l in lines for it in l]) == H.canonical(R.ref_build_dump(cfg, t, 2).items)
+
+
+@pytest.mark.skipif(not R.ref_available(), reason="oracle/_ref not built")
+@pytest.mark.parametrize("d,k", [(96, 4), (64, 1), (130, 2)])
+def test_block_diag_split_and_flops_match_reference(d, k):
+    """kfac.block_diag_split_factor / inversion_flops / block_diag_inversion_flops
+    vs the compiled reference (kfac.cpp:203-226), bit-exact; K must divide d."""
+    import torch
+    from paper_2211_14133_b200 import kfac as K
+    m = R.orc_symmetric(7 + d, (d, d))
+    blocks, ff, fb = R.ref_block_diag_split(m, k)
+    ours = K.block_diag_split_factor(torch.from_numpy(m), k)
+    assert len(ours) == k and all(np.array_equal(b, o.numpy()) for b, o in zip(blocks, ours))
+    assert K.inversion_flops(d) == ff and K.block_diag_inversion_flops(d, k) == fb
+    with pytest.raises(ValueError):
+        K.block_diag_split_factor(torch.from_numpy(m), 7)

@@ -384,3 +384,29 @@ def test_custom_queue_with_measured_durations():
               if w.kind in (S.WorkKind.Curvature, S.WorkKind.Inversion)]
     assert len(placed) == len(q.items)
     assert sorted(w.duration for w in placed) == sorted(w.duration for w in q.items)
+
+
+def _canon_events(doc):
+    return sorted(doc["traceEvents"], key=lambda e: (e["tid"], e["ts"], e["name"], e["dur"]))
+
+
+@pytest.mark.parametrize("name", ["gpipe_d2n2_hand", "chimera_d4n4_l4_serial", "1f1b_d4n8_recompute"])
+def test_schedule_trace_matches_reference_trace_to_json(name):
+    """engine.schedule_trace == the reference's io::trace_to_json
+    (proj/src/io/trace.cpp:38-63) on the same assigned schedule: event names,
+    ts/dur in us (llround), pid/tid, args — compared after a canonical order
+    (the reference's final std::sort is unstable on ties).  Golden: the
+    compiled reference (tests/golden/make_golden.py)."""
+    from paper_2211_14133_b200.engine import schedule_trace
+    here = os.path.join(os.path.dirname(__file__), "golden")
+    gold = json.load(open(os.path.join(here, "traces.json")))[name]
+    g = json.load(open(GOLDEN))[name]
+    cfg = S.PipelineConfig(method=S.Method(g["config"]["method"]), stages=g["config"]["stages"],
+                           micro_batches=g["config"]["micro_batches"],
+                           micro_batch_size=g["config"]["micro_batch_size"], replicas=g["config"]["replicas"],
+                           devices=g["config"]["devices"], layers_per_stage=g["config"]["layers_per_stage"],
+                           seq_len=g["config"]["seq_len"], recompute=bool(g["config"]["recompute"]))
+    costs = S.CostTable(**{k: (float.fromhex(v) if isinstance(v, str) else v) for k, v in g["costs"].items()})
+    filled = product_assign(cfg, costs, g["inversion_parallel"], g["horizon_cap"])
+    ours = schedule_trace(filled.schedule, gold["devices_per_group"])
+    assert _canon_events(ours) == _canon_events(gold["trace"])
