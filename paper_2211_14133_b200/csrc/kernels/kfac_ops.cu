@@ -355,6 +355,11 @@ struct InvWs {
     void* side0[8] = {};
     void* side1[8] = {};
     int t_row[8] = {};  // row of w.t where the depth's T^T lives (ld = w.ld)
+    // right-looking factorisation: per-panel digit slots (3-deep ring) for the
+    // A panel, the leaf inverse X_kk and the L panel
+    void* pa[3] = {};
+    void* px[3] = {};
+    void* pl[3] = {};
     int* info = nullptr;
 };
 
@@ -371,7 +376,7 @@ std::vector<int> node_n1_bounds(int d) {
 int t_rows(int d) {
     int r = 0;
     for (int n1 : node_n1_bounds(d)) r += n1;
-    return std::max(r, 1);
+    return std::max(r, d);  // >= d: the bottom-up TRTRI keeps T^T of node (o, n) at rows [o, o + n1)
 }
 
 size_t inverse_ws_bytes(int d) {
@@ -379,7 +384,8 @@ size_t inverse_ws_bytes(int d) {
     const size_t tplane = align256(static_cast<size_t>(round_up(d, 4)) * t_rows(d) * sizeof(float));
     size_t side = 0;
     for (int n1 : node_n1_bounds(d)) side += 2 * align256(sliced_bytes(n1, n1));
-    return 4 * plane + tplane + 2 * align256(sliced_bytes(d, d)) + side;
+    const size_t panel = 2 * align256(sliced_bytes(d, kLeaf)) + align256(sliced_bytes(kLeaf, kLeaf));
+    return 4 * plane + tplane + 2 * align256(sliced_bytes(d, d)) + side + 3 * panel;
 }
 
 InvWs carve(void* base, int d) {
@@ -405,6 +411,14 @@ InvWs carve(void* base, int d) {
         q += align256(sliced_bytes(b[k], b[k]));
         w.t_row[k] = row;  // T^T of a depth-k node: n1 <= b[k] rows
         row += b[k];
+    }
+    for (int i = 0; i < 3; ++i) {
+        w.pa[i] = q;
+        q += align256(sliced_bytes(d, kLeaf));
+        w.pl[i] = q;
+        q += align256(sliced_bytes(d, kLeaf));
+        w.px[i] = q;
+        q += align256(sliced_bytes(kLeaf, kLeaf));
     }
     return w;
 }
@@ -436,12 +450,12 @@ struct SideSlot {
 };
 
 SideSlot& side_slot(int group, int depth) {
-    thread_local std::vector<std::vector<SideSlot>> pools;  // [device][group * 8 + depth]
+    thread_local std::vector<std::vector<SideSlot>> pools;  // [device][group * 16 + slot]
     int dev = 0;
     check(cudaGetDevice(&dev), "cudaGetDevice");
     if (pools.size() <= static_cast<std::size_t>(dev)) pools.resize(dev + 1);
     auto& v = pools[dev];
-    const std::size_t i = static_cast<std::size_t>(group) * 8 + depth;
+    const std::size_t i = static_cast<std::size_t>(group) * 16 + depth;
     if (v.size() <= i) v.resize(i + 1);
     SideSlot& sl = v[i];
     if (!sl.stream) {
@@ -718,6 +732,237 @@ void inverse_rec(const std::vector<InvWs>& ws, int o, int n, Emitter& em, int de
     em.gemms(g);
 }
 
+// ------------------------------------------------------------ right-looking Cholesky + TRTRI
+// Side-slot indices: 0..7 the TRTRI depths, 8..10 the panel ring.
+constexpr int kPanelSlot = 8;
+
+// Blocked right-looking Cholesky with look-ahead, 128-column panels.  Per
+// panel k the CRITICAL path is: leaf (L_kk, X_kk) -> TRSM of the rows below,
+// L[>k, k] = A[>k, k] X_kk^T (one GEMM) -> update of block column k+1 only
+// (look-ahead) -> leaf k+1.  The rest of the trailing update (columns >= k+2,
+// lower) runs on a side stream and is joined before the next look-ahead
+// (both read-modify-write block column k+2).  w.l receives the strictly-lower
+// L, w.x / w.xt the diagonal blocks of L^-1.
+void cholesky_blocked(const std::vector<InvWs>& ws, Emitter& em) {
+    const int d = ws.front().d;
+    const int nb = (d + kLeaf - 1) / kLeaf;
+    for (int k = 0; k < nb; ++k) {
+        const int o = k * kLeaf;
+        em.leaves(ws, o, std::min(kLeaf, d - o));
+        if (k == nb - 1) break;
+        const int r0 = o + kLeaf, m = d - r0, slot = k % 3;
+        std::vector<SliceReq> sl;
+        std::vector<GemmSpec> g;
+        // ---- TRSM: L[r0:, k] = A[r0:, k] X_kk^T
+        for (const InvWs& w : ws) {
+            sl.push_back(slice_of(w.a, w.ld, r0, o, m, kLeaf, w.pa[slot], SLICE_FULL));
+            sl.push_back(slice_of(w.x, w.ld, o, o, kLeaf, kLeaf, w.px[slot], SLICE_FULL));
+            GemmSpec t;
+            t.a = sliced_view(w.pa[slot], m, kLeaf);
+            t.b = sliced_view(w.px[slot], kLeaf, kLeaf);
+            t.rows = m;
+            t.cols = kLeaf;
+            t.k = kLeaf;
+            t.flags = EPI_VEC4;
+            t.c = at(w.l, w.ld, r0, o);
+            t.ldc = w.ld;
+            g.push_back(t);
+        }
+        em.slices(sl);
+        em.gemms(g);
+        sl.clear();
+        g.clear();
+        for (const InvWs& w : ws) sl.push_back(slice_of(w.l, w.ld, r0, o, m, kLeaf, w.pl[slot], SLICE_FULL));
+        em.slices(sl);
+        if (k >= 1) em.side_join(kPanelSlot + (k - 1) % 3);  // bulk(k-1) also writes block column k+1
+        // ---- look-ahead: A[r0:, k+1] -= L[r0:, k] L[k+1, k]^T
+        const int nc = std::min(kLeaf, m);
+        for (const InvWs& w : ws) {
+            const Sliced lp = sliced_view(w.pl[slot], m, kLeaf);
+            GemmSpec u;
+            u.a = lp;
+            u.b = rows_of(lp, 0, nc);
+            u.rows = m;
+            u.cols = nc;
+            u.k = kLeaf;
+            u.alpha = -1.0f;
+            u.beta = 1.0f;
+            u.flags = EPI_VEC4;
+            u.c = at(w.a, w.ld, r0, r0);
+            u.ldc = w.ld;
+            g.push_back(u);
+        }
+        em.gemms(g);
+        // ---- bulk: A[r0+128:, r0+128:] -= L[r0+128:, k] L[r0+128:, k]^T  (lower), side stream
+        if (m > kLeaf) {
+            em.side_begin(kPanelSlot + slot);
+            g.clear();
+            for (const InvWs& w : ws) {
+                const Sliced lb = rows_of(sliced_view(w.pl[slot], m, kLeaf), kLeaf, m - kLeaf);
+                GemmSpec b;
+                b.a = lb;
+                b.b = lb;
+                b.rows = b.cols = m - kLeaf;
+                b.k = kLeaf;
+                b.lower = true;
+                b.alpha = -1.0f;
+                b.beta = 1.0f;
+                b.flags = EPI_VEC4;
+                b.c = at(w.a, w.ld, r0 + kLeaf, r0 + kLeaf);
+                b.ldc = w.ld;
+                g.push_back(b);
+            }
+            em.gemms(g);
+            em.side_end(kPanelSlot + slot);
+        }
+    }
+}
+
+// X = L^-1 from the strictly-lower L (w.l) and the leaves' diagonal blocks:
+// per node X21 = -X22 (L21 X11); T^T = (L21 X11)^T needs only the left half,
+// so it runs on the depth's side stream while the right half is inverted.
+void trtri_rec(const std::vector<InvWs>& ws, int o, int n, Emitter& em, int depth = 0) {
+    if (n <= kLeaf) return;  // diagonal block inverted by its leaf
+    const int n1 = kTile * ((n + 2 * kTile - 1) / (2 * kTile));
+    const int n2 = n - n1;
+    trtri_rec(ws, o, n1, em, depth + 1);
+    std::vector<SliceReq> sl;
+    std::vector<GemmSpec> g;
+    em.side_begin(depth);
+    for (const InvWs& w : ws) {
+        sl.push_back(slice_of(w.l, w.ld, o + n1, o, n2, n1, w.side0[depth], SLICE_FULL));
+        sl.push_back(slice_of(w.xt, w.ld, o, o, n1, n1, w.side1[depth], SLICE_UPPER_BLOCK));
+        GemmSpec s;
+        s.a = sliced_view(w.side0[depth], n2, n1);
+        s.b = sliced_view(w.side1[depth], n1, n1);
+        s.rows = n2;
+        s.cols = n1;
+        s.k = n1;
+        s.k_mode = K_FROM_COL_TILE;
+        s.flags = EPI_TRANSPOSE;
+        s.c = at(w.t, w.ld, w.t_row[depth], 0);  // T^T [n1 x n2]
+        s.ldc = w.ld;
+        g.push_back(s);
+    }
+    em.slices(sl);
+    em.gemms(g);
+    em.side_end(depth);
+    trtri_rec(ws, o + n1, n2, em, depth + 1);
+    em.side_join(depth);
+    sl.clear();
+    g.clear();
+    for (const InvWs& w : ws) {
+        sl.push_back(slice_of(w.x, w.ld, o + n1, o + n1, n2, n2, w.s0, SLICE_LOWER_BLOCK));
+        sl.push_back(slice_of(w.t, w.ld, w.t_row[depth], 0, n1, n2, w.s1, SLICE_FULL));
+        GemmSpec s;
+        s.a = sliced_view(w.s0, n2, n2);
+        s.b = sliced_view(w.s1, n1, n2);
+        s.rows = n2;
+        s.cols = n1;
+        s.k = n2;
+        s.k_mode = K_TO_ROW_TILE_END;
+        s.alpha = -1.0f;
+        s.flags = EPI_ALSO_T | EPI_VEC4;
+        s.c = at(w.x, w.ld, o + n1, o);
+        s.ldc = w.ld;
+        s.c_t = at(w.xt, w.ld, o, o + n1);
+        s.ldc_t = w.ld;
+        g.push_back(s);
+    }
+    em.slices(sl);
+    em.gemms(g);
+}
+
+// X = L^-1 bottom-up: the recursion tree of node splits (n1 = 128 ceil(n/256))
+// grouped by height; every node of a height is independent, so each height is
+// four batched launches (slices, T^T GEMMs, slices, X21 GEMMs) over all its
+// nodes instead of a depth-first chain.  Same arithmetic per node as trtri_rec.
+// Scratch: T^T of node (o, n) at rows [o, o + n1) of w.t (disjoint within a
+// height); digit blocks packed in s0 / s1 (L21 | X22) and side0/side1 (XT11 | T).
+struct TriNode {
+    int o, n1, n2;
+};
+
+int tri_height(int n, std::vector<std::vector<TriNode>>& by_h, int o) {
+    if (n <= kLeaf) return 0;
+    const int n1 = kTile * ((n + 2 * kTile - 1) / (2 * kTile));
+    const int h = 1 + std::max(tri_height(n1, by_h, o), tri_height(n - n1, by_h, o + n1));
+    if (static_cast<int>(by_h.size()) < h) by_h.resize(h);
+    by_h[h - 1].push_back(TriNode{o, n1, n - n1});
+    return h;
+}
+
+void trtri_levels(const std::vector<InvWs>& ws, Emitter& em) {
+    const int d = ws.front().d;
+    std::vector<std::vector<TriNode>> by_h;
+    tri_height(d, by_h, 0);
+    for (const auto& level : by_h) {
+        std::vector<SliceReq> sl;
+        std::vector<GemmSpec> g;
+        for (const InvWs& w : ws) {
+            size_t off0 = 0, off1 = 0;
+            for (const TriNode& nd : level) {
+                char* a = static_cast<char*>(w.s0) + off0;
+                char* b = static_cast<char*>(w.s1) + off1;
+                off0 += align256(sliced_bytes(nd.n2, nd.n1));
+                off1 += align256(sliced_bytes(nd.n1, nd.n1));
+                sl.push_back(slice_of(w.l, w.ld, nd.o + nd.n1, nd.o, nd.n2, nd.n1, a, SLICE_FULL));
+                sl.push_back(slice_of(w.xt, w.ld, nd.o, nd.o, nd.n1, nd.n1, b, SLICE_UPPER_BLOCK));
+                GemmSpec s;
+                s.a = sliced_view(a, nd.n2, nd.n1);
+                s.b = sliced_view(b, nd.n1, nd.n1);
+                s.rows = nd.n2;
+                s.cols = nd.n1;
+                s.k = nd.n1;
+                s.k_mode = K_FROM_COL_TILE;
+                s.flags = EPI_TRANSPOSE;
+                s.c = at(w.t, w.ld, nd.o, 0);  // T^T [n1 x n2]
+                s.ldc = w.ld;
+                g.push_back(s);
+            }
+        }
+        em.slices(sl);
+        em.gemms(g);
+        sl.clear();
+        g.clear();
+        for (const InvWs& w : ws) {
+            size_t off0 = 0, off1 = 0;
+            for (const TriNode& nd : level) {
+                char* a = static_cast<char*>(w.side0[0]) + off0;
+                char* b = static_cast<char*>(w.side1[0]) + off1;
+                off0 += align256(sliced_bytes(nd.n2, nd.n2));
+                off1 += align256(sliced_bytes(nd.n1, nd.n2));
+                sl.push_back(slice_of(w.x, w.ld, nd.o + nd.n1, nd.o + nd.n1, nd.n2, nd.n2, a, SLICE_LOWER_BLOCK));
+                sl.push_back(slice_of(w.t, w.ld, nd.o, 0, nd.n1, nd.n2, b, SLICE_FULL));
+                GemmSpec s;
+                s.a = sliced_view(a, nd.n2, nd.n2);
+                s.b = sliced_view(b, nd.n1, nd.n2);
+                s.rows = nd.n2;
+                s.cols = nd.n1;
+                s.k = nd.n2;
+                s.k_mode = K_TO_ROW_TILE_END;
+                s.alpha = -1.0f;
+                s.flags = EPI_ALSO_T | EPI_VEC4;
+                s.c = at(w.x, w.ld, nd.o + nd.n1, nd.o);
+                s.ldc = w.ld;
+                s.c_t = at(w.xt, w.ld, nd.o, nd.o + nd.n1);
+                s.ldc_t = w.ld;
+                g.push_back(s);
+            }
+        }
+        em.slices(sl);
+        em.gemms(g);
+    }
+}
+
+bool use_recursive_inverse() {
+    static const bool on = [] {
+        const char* e = std::getenv("PF_INV_RECURSIVE");
+        return e && e[0] == '1';
+    }();
+    return on;
+}
+
 void damped_inverse_group(const std::vector<const pf_inverse_problem*>& probs, Emitter& em) {
     const int d = probs.front()->d;
     std::vector<InvWs> ws;
@@ -729,7 +974,12 @@ void damped_inverse_group(const std::vector<const pf_inverse_problem*>& probs, E
         ws.push_back(w);
     }
     em.damp(damps);
-    inverse_rec(ws, 0, d, em);
+    if (use_recursive_inverse()) {
+        inverse_rec(ws, 0, d, em);
+    } else {
+        cholesky_blocked(ws, em);
+        trtri_levels(ws, em);
+    }
     // ---- LAUUM: M^-1 = X^T X = XT XT^T  (lower tiles, mirrored)
     std::vector<SliceReq> sl;
     std::vector<GemmSpec> g;
