@@ -955,15 +955,24 @@ void trtri_levels(const std::vector<InvWs>& ws, Emitter& em) {
     }
 }
 
-bool use_recursive_inverse() {
-    static const bool on = [] {
+// Two schedules of the same factorisation: the right-looking one (above) has
+// the shortest critical path but re-reads / re-writes the trailing matrix once
+// per 128-column panel (K = 128 updates); the recursive one (inverse_rec)
+// aggregates those updates into large-K GEMMs.  A call with few factors is
+// latency-bound (right-looking wins: one BERT-Large layer, 3.5 -> 3.1 ms for
+// the two d = 4096 factors); a call with many is throughput-bound (recursive
+// wins: a 24-layer refresh, 60 -> 37 ms).  PF_INV_RECURSIVE=0/1 forces one.
+int g_recursive_from = 24;  // problems per call at which the recursive schedule takes over
+
+bool use_recursive_inverse(int problems) {
+    static const int forced = [] {
         const char* e = std::getenv("PF_INV_RECURSIVE");
-        return e && e[0] == '1';
+        return e ? (e[0] == '1' ? 1 : 0) : -1;
     }();
-    return on;
+    return forced >= 0 ? forced == 1 : problems >= g_recursive_from;
 }
 
-void damped_inverse_group(const std::vector<const pf_inverse_problem*>& probs, Emitter& em) {
+void damped_inverse_group(const std::vector<const pf_inverse_problem*>& probs, Emitter& em, bool recursive) {
     const int d = probs.front()->d;
     std::vector<InvWs> ws;
     std::vector<Damp2D> damps;
@@ -974,7 +983,7 @@ void damped_inverse_group(const std::vector<const pf_inverse_problem*>& probs, E
         ws.push_back(w);
     }
     em.damp(damps);
-    if (use_recursive_inverse()) {
+    if (recursive) {
         inverse_rec(ws, 0, d, em);
     } else {
         cholesky_blocked(ws, em);
@@ -1032,6 +1041,8 @@ std::size_t put_bytes(std::vector<uint8_t>& buf, const V& v, std::size_t align) 
 }
 
 GraphProg* build_program(const std::vector<std::vector<const pf_inverse_problem*>>& groups, cudaStream_t st) {
+    int n_problems = 0;
+    for (const auto& g : groups) n_problems += static_cast<int>(g.size());
     std::vector<GemmDesc> gemms;
     std::vector<CUtensorMap> maps;
     std::vector<SliceJob> slice_jobs;
@@ -1045,7 +1056,7 @@ GraphProg* build_program(const std::vector<std::vector<const pf_inverse_problem*
         b.slice_jobs = &slice_jobs;
         b.leaf_jobs = &leaf_jobs;
         b.damp_jobs = &damp_jobs;
-        damped_inverse_group(groups[gi], b);
+        damped_inverse_group(groups[gi], b, use_recursive_inverse(n_problems));
     }
     // interleave the chains phase by phase: round r holds phase r of every
     // group, so a task only ever waits on lower-indexed tasks
@@ -1422,12 +1433,13 @@ int pf_damped_inverse_batched(const pf_inverse_problem* problems, int count, voi
             i = j;
         }
         const cudaStream_t st = static_cast<cudaStream_t>(stream);
+        const bool recursive = use_recursive_inverse(count);
         if (g_inverse_mode.load() == 1) {
             run_program(groups, st);  // one persistent launch for every group
         } else {
             run_forked(groups.size(), st, [&](std::size_t g, cudaStream_t s) {
                 StreamEmitter em(s, static_cast<int>(g));
-                damped_inverse_group(groups[g], em);
+                damped_inverse_group(groups[g], em, recursive);
             });
         }
         return 0;

@@ -355,3 +355,17 @@ def test_kfac_state_block_diag_refresh(K):
     a = st.inv_a[0].fp32
     assert torch.all(a[:128, 128:] == 0) and torch.all(a[128:, :128] == 0)
     assert st.has_inverses(0) and st.staleness[0] == 0
+
+
+def test_large_batch_uses_recursive_schedule_and_matches_oracle(K):
+    """>= 24 factors per call switch to the throughput schedule (recursive
+    blocked Cholesky); every inverse still matches the FP64 oracle."""
+    sizes = [300, 256, 129] * 8  # 24 problems
+    ms = [spd(1200 + i, d) for i, d in enumerate(sizes)]
+    ts = [torch.from_numpy(m).float().cuda() for m in ms]
+    outs = K.damped_inverse_batched(ts, 0.1)
+    for m, o in zip(ms, outs):
+        m32 = m.astype(np.float32).astype(np.float64)
+        got = o.double().cpu().numpy()
+        assert rel_fro(got, R.orc_cholesky_spd_inverse(m32, 0.1)) <= 1e-4
+        assert residual(m32, got, 0.1) <= INV_RESIDUAL_TOL
