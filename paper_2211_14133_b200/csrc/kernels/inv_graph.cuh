@@ -199,7 +199,7 @@ __device__ __noinline__ void graph_gemm_tile(const GraphProgram& g, int di, int 
         const int ew = warp & 3, half = warp >> 2;
         epilogue_chunks<kOZ8>(P, tm, tn, tmem + (static_cast<uint32_t>(ew * 32) << 16),
                               tm * kTile + ew * 32 + static_cast<int>(lane), col_scale, 4 * half, 4 * half + 4,
-                              kb1 > kb0);
+                              kb1 > kb0, epi_row<kOZ8>(P, tm, tn, tm * kTile + ew * 32 + static_cast<int>(lane)));
     }
     ptx::tc_fence_before();
     if (tid == 0 && tr) tr[7] = global_ns();

@@ -60,6 +60,34 @@ bool pdl_enabled() {
     return on;
 }
 
+// Launch priority of the next launches (cudaLaunchAttributePriority; 0 = the
+// stream's own).  The inversion marks its critical chain high and its side
+// branches low, so that when a wide side GEMM holds every SM the block
+// scheduler hands the next free SM to the critical kernel.  PF_NO_PRIO=1
+// disables (A/B measurement).
+thread_local int g_launch_prio = 0;
+
+bool prio_enabled() {
+    static const bool on = [] {
+        const char* e = std::getenv("PF_NO_PRIO");
+        return !(e && e[0] == '1');
+    }();
+    return on;
+}
+
+// (least, greatest) of the device's priority range, e.g. (0, -5)
+std::pair<int, int> prio_range() {
+    int least = 0, greatest = 0;
+    check(cudaDeviceGetStreamPriorityRange(&least, &greatest), "cudaDeviceGetStreamPriorityRange");
+    return {least, greatest};
+}
+
+struct ScopedPrio {
+    int saved;
+    explicit ScopedPrio(int p) : saved(g_launch_prio) { g_launch_prio = prio_enabled() ? p : 0; }
+    ~ScopedPrio() { g_launch_prio = saved; }
+};
+
 template <typename... KArgs, typename... Args>
 void launch(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t st,
             Args&&... args) {
@@ -68,11 +96,20 @@ void launch(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaSt
     cfg.blockDim = block;
     cfg.dynamicSmemBytes = smem;
     cfg.stream = st;
-    cudaLaunchAttribute attr[1];
-    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cudaLaunchAttribute attr[2];
+    int na = 0;
+    if (pdl_enabled()) {
+        attr[na].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+        attr[na].val.programmaticStreamSerializationAllowed = 1;
+        ++na;
+    }
+    if (g_launch_prio != 0) {
+        attr[na].id = cudaLaunchAttributePriority;
+        attr[na].val.priority = g_launch_prio;
+        ++na;
+    }
     cfg.attrs = attr;
-    cfg.numAttrs = pdl_enabled() ? 1 : 0;
+    cfg.numAttrs = na;
     check(cudaLaunchKernelEx(&cfg, kernel, std::forward<Args>(args)...), "cudaLaunchKernelEx");
 }
 
@@ -440,6 +477,13 @@ struct Emitter {
     virtual void side_begin(int) {}
     virtual void side_end(int) {}
     virtual void side_join(int) {}
+    // explicit stream/event form for DAGs the fork/join pairs cannot express:
+    // on(s) directs what follows to stream s (0 = main), record(e) / wait(e)
+    // mark and await event e.  Program order must itself be a valid
+    // sequential order (the persistent back end ignores all three).
+    virtual void on(int) {}
+    virtual void record(int) {}
+    virtual void wait(int) {}
 };
 
 // Per-thread, per-device pool of (stream, done event) pairs for the side
@@ -466,6 +510,18 @@ SideSlot& side_slot(int group, int depth) {
     return sl;
 }
 
+cudaEvent_t pool_event(int group, int id) {
+    thread_local std::vector<std::vector<cudaEvent_t>> pools;  // [device][group * 16 + id]
+    int dev = 0;
+    check(cudaGetDevice(&dev), "cudaGetDevice");
+    if (pools.size() <= static_cast<std::size_t>(dev)) pools.resize(dev + 1);
+    auto& v = pools[dev];
+    const std::size_t i = static_cast<std::size_t>(group) * 16 + id;
+    if (v.size() <= i) v.resize(i + 1, nullptr);
+    if (!v[i]) check(cudaEventCreateWithFlags(&v[i], cudaEventDisableTiming), "cudaEventCreate(pool)");
+    return v[i];
+}
+
 LeafArgs leaf_args(const InvWs& w, int o, int n) {
     return LeafArgs{at(w.a, w.ld, o, o), at(w.x, w.ld, o, o), at(w.xt, w.ld, o, o), w.info, w.ld, n, o};
 }
@@ -479,21 +535,34 @@ struct StreamEmitter final : Emitter {
     cudaStream_t st;
     cudaStream_t main;
     int group;
-    explicit StreamEmitter(cudaStream_t s, int g = 0) : st(s), main(s), group(g) {}
+    int prio_main, prio_side, prio;  // launch priorities: critical chain high, side branches low
+    explicit StreamEmitter(cudaStream_t s, int g = 0) : st(s), main(s), group(g) {
+        const auto [least, greatest] = prio_range();
+        prio_main = prio = greatest;
+        prio_side = least;
+    }
     void side_begin(int depth) override {
         SideSlot& sl = side_slot(group, depth);
         check(cudaEventRecord(sl.fork, main), "cudaEventRecord(side fork)");
         check(cudaStreamWaitEvent(sl.stream, sl.fork, 0), "side fork");
         st = sl.stream;
+        prio = prio_side;
     }
     void side_end(int depth) override {
         SideSlot& sl = side_slot(group, depth);
         check(cudaEventRecord(sl.done, sl.stream), "cudaEventRecord(side done)");
         st = main;
+        prio = prio_main;
     }
     void side_join(int depth) override {
         check(cudaStreamWaitEvent(main, side_slot(group, depth).done, 0), "side join");
     }
+    void on(int s) override {
+        st = s == 0 ? main : side_slot(group, 11 + s).stream;
+        prio = s == 0 ? prio_main : prio_side;
+    }
+    void record(int e) override { check(cudaEventRecord(pool_event(group, e), st), "cudaEventRecord(pool)"); }
+    void wait(int e) override { check(cudaStreamWaitEvent(st, pool_event(group, e), 0), "cudaStreamWaitEvent(pool)"); }
     void damp(const std::vector<Damp2D>& jobs) override {
         DampBatch db{};
         int d = 1;
@@ -501,12 +570,20 @@ struct StreamEmitter final : Emitter {
             db.e[i] = jobs[i];
             d = std::max(d, jobs[i].d);
         }
+        ScopedPrio sp(prio);
         launch(damp_kernel, dim3((d + 7) / 8, static_cast<unsigned>(jobs.size())), dim3(256), 0, st, db);
         after_launch("damp_kernel");
     }
-    void slices(const std::vector<SliceReq>& reqs) override { launch_slices(reqs, st); }
-    void gemms(const std::vector<GemmSpec>& specs) override { gemm_oz8(specs, st); }
+    void slices(const std::vector<SliceReq>& reqs) override {
+        ScopedPrio sp(prio);
+        launch_slices(reqs, st);
+    }
+    void gemms(const std::vector<GemmSpec>& specs) override {
+        ScopedPrio sp(prio);
+        gemm_oz8(specs, st);
+    }
     void leaves(const std::vector<InvWs>& ws, int o, int n) override {
+        ScopedPrio sp(prio);
         static std::once_flag once;
         std::call_once(once, [] {
             check(cudaFuncSetAttribute(leaf_chol_inv_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -733,30 +810,63 @@ void inverse_rec(const std::vector<InvWs>& ws, int o, int n, Emitter& em, int de
 }
 
 // ------------------------------------------------------------ right-looking Cholesky + TRTRI
-// Side-slot indices: 0..7 the TRTRI depths, 8..10 the panel ring.
-constexpr int kPanelSlot = 8;
+// Side-slot indices: 0..7 the TRTRI depths, 12..13 the panel side streams (on(1), on(2)).
 
-// Blocked right-looking Cholesky with look-ahead, 128-column panels.  Per
-// panel k the CRITICAL path is: leaf (L_kk, X_kk) -> TRSM of the rows below,
-// L[>k, k] = A[>k, k] X_kk^T (one GEMM) -> update of block column k+1 only
-// (look-ahead) -> leaf k+1.  The rest of the trailing update (columns >= k+2,
-// lower) runs on a side stream and is joined before the next look-ahead
-// (both read-modify-write block column k+2).  w.l receives the strictly-lower
-// L, w.x / w.xt the diagonal blocks of L^-1.
+// Blocked right-looking Cholesky with a two-level look-ahead, 128-column
+// panels.  Per panel k the CRITICAL chain (main stream) is
+//   leaf(k) -> slice X_kk -> TRSM L[>k, k] = A[>k, k] X_kk^T -> slice L
+//   -> A[k+1, k+1] -= L[k+1, k] L[k+1, k]^T (one tile) -> leaf(k+1)
+// and everything else runs on two alternating side streams R(k % 2):
+//   col  A[>k+1, k+1] -= L[>k+1, k] L[k+1, k]^T, then slice that column
+//        (the A panel of k+1, awaited before TRSM(k+1))      -> event A
+//   BU   block column k+2 (awaited by the diagonal update and col of k+1) -> U
+//   BR   the rest, columns >= k+3, lower (awaited by BU(k+1))             -> B
+// so the trailing update overlaps leaf(k+1) instead of preceding it.
+// w.l receives the strictly-lower L, w.x / w.xt the diagonal blocks of L^-1.
 void cholesky_blocked(const std::vector<InvWs>& ws, Emitter& em) {
     const int d = ws.front().d;
     const int nb = (d + kLeaf - 1) / kLeaf;
+    // event ids (per group, 16 available): F fork, A/U/B rings of 2, END per side stream
+    auto evA = [](int k) { return 1 + (k & 1); };
+    auto evU = [](int k) { return 3 + (k & 1); };
+    auto evB = [](int k) { return 5 + (k & 1); };
+    constexpr int evF = 0, evEnd0 = 7;
+    auto update = [](const InvWs& w, const Sliced& a, const Sliced& b, int rows, int cols, int r, int c,
+                     bool lower) {
+        GemmSpec u;
+        u.a = a;
+        u.b = b;
+        u.rows = rows;
+        u.cols = cols;
+        u.k = kLeaf;
+        u.lower = lower;
+        u.alpha = -1.0f;
+        u.beta = 1.0f;
+        u.flags = EPI_VEC4;
+        u.c = at(w.a, w.ld, r, c);
+        u.ldc = w.ld;
+        return u;
+    };
+    std::vector<SliceReq> sl;
+    std::vector<GemmSpec> g;
+    if (nb > 1) {  // A panel of panel 0
+        for (const InvWs& w : ws) sl.push_back(slice_of(w.a, w.ld, kLeaf, 0, d - kLeaf, kLeaf, w.pa[0], SLICE_FULL));
+        em.slices(sl);
+    }
+    bool side_used[2] = {false, false};
     for (int k = 0; k < nb; ++k) {
         const int o = k * kLeaf;
         em.leaves(ws, o, std::min(kLeaf, d - o));
         if (k == nb - 1) break;
         const int r0 = o + kLeaf, m = d - r0, slot = k % 3;
-        std::vector<SliceReq> sl;
-        std::vector<GemmSpec> g;
+        const int nc = std::min(kLeaf, m);  // width of block column k+1
+        sl.clear();
+        g.clear();
+        for (const InvWs& w : ws) sl.push_back(slice_of(w.x, w.ld, o, o, kLeaf, kLeaf, w.px[slot], SLICE_FULL));
+        em.slices(sl);
+        if (k >= 1) em.wait(evA(k));  // A panel of k (col of k-1)
         // ---- TRSM: L[r0:, k] = A[r0:, k] X_kk^T
         for (const InvWs& w : ws) {
-            sl.push_back(slice_of(w.a, w.ld, r0, o, m, kLeaf, w.pa[slot], SLICE_FULL));
-            sl.push_back(slice_of(w.x, w.ld, o, o, kLeaf, kLeaf, w.px[slot], SLICE_FULL));
             GemmSpec t;
             t.a = sliced_view(w.pa[slot], m, kLeaf);
             t.b = sliced_view(w.px[slot], kLeaf, kLeaf);
@@ -768,53 +878,69 @@ void cholesky_blocked(const std::vector<InvWs>& ws, Emitter& em) {
             t.ldc = w.ld;
             g.push_back(t);
         }
-        em.slices(sl);
         em.gemms(g);
         sl.clear();
         g.clear();
         for (const InvWs& w : ws) sl.push_back(slice_of(w.l, w.ld, r0, o, m, kLeaf, w.pl[slot], SLICE_FULL));
         em.slices(sl);
-        if (k >= 1) em.side_join(kPanelSlot + (k - 1) % 3);  // bulk(k-1) also writes block column k+1
-        // ---- look-ahead: A[r0:, k+1] -= L[r0:, k] L[k+1, k]^T
-        const int nc = std::min(kLeaf, m);
-        for (const InvWs& w : ws) {
-            const Sliced lp = sliced_view(w.pl[slot], m, kLeaf);
-            GemmSpec u;
-            u.a = lp;
-            u.b = rows_of(lp, 0, nc);
-            u.rows = m;
-            u.cols = nc;
-            u.k = kLeaf;
-            u.alpha = -1.0f;
-            u.beta = 1.0f;
-            u.flags = EPI_VEC4;
-            u.c = at(w.a, w.ld, r0, r0);
-            u.ldc = w.ld;
-            g.push_back(u);
-        }
-        em.gemms(g);
-        // ---- bulk: A[r0+128:, r0+128:] -= L[r0+128:, k] L[r0+128:, k]^T  (lower), side stream
-        if (m > kLeaf) {
-            em.side_begin(kPanelSlot + slot);
-            g.clear();
+        if (k >= 1 && m > 0) em.wait(evU(k - 1));  // BU(k-1) wrote block column k+1
+        const bool rest = m > kLeaf;
+        const int side = 1 + (k & 1);
+        if (rest) {
+            em.record(evF);
+            em.on(side);
+            em.wait(evF);
+            side_used[side - 1] = true;
+            const int m2 = m - kLeaf;  // rows below block k+1
+            // col: A[r0+128:, k+1] -= L[r0+128:, k] L[k+1, k]^T, then the A panel of k+1
             for (const InvWs& w : ws) {
-                const Sliced lb = rows_of(sliced_view(w.pl[slot], m, kLeaf), kLeaf, m - kLeaf);
-                GemmSpec b;
-                b.a = lb;
-                b.b = lb;
-                b.rows = b.cols = m - kLeaf;
-                b.k = kLeaf;
-                b.lower = true;
-                b.alpha = -1.0f;
-                b.beta = 1.0f;
-                b.flags = EPI_VEC4;
-                b.c = at(w.a, w.ld, r0 + kLeaf, r0 + kLeaf);
-                b.ldc = w.ld;
-                g.push_back(b);
+                const Sliced lp = sliced_view(w.pl[slot], m, kLeaf);
+                g.push_back(update(w, rows_of(lp, kLeaf, m2), rows_of(lp, 0, nc), m2, nc, r0 + kLeaf, r0, false));
             }
             em.gemms(g);
-            em.side_end(kPanelSlot + slot);
+            g.clear();
+            sl.clear();
+            const int ns = (k + 1) % 3;
+            for (const InvWs& w : ws) sl.push_back(slice_of(w.a, w.ld, r0 + kLeaf, r0, m2, kLeaf, w.pa[ns], SLICE_FULL));
+            em.slices(sl);
+            em.record(evA(k + 1));
+            // BU: block column k+2 (rows >= k+2) -- BR(k-1) also wrote it
+            if (k >= 1) em.wait(evB(k - 1));
+            const int nc2 = std::min(kLeaf, m2);
+            for (const InvWs& w : ws) {
+                const Sliced lb = rows_of(sliced_view(w.pl[slot], m, kLeaf), kLeaf, m2);
+                g.push_back(update(w, lb, rows_of(lb, 0, nc2), m2, nc2, r0 + kLeaf, r0 + kLeaf, false));
+            }
+            em.gemms(g);
+            g.clear();
+            em.record(evU(k));
+            // BR: columns >= k+3, lower
+            const int m3 = m2 - kLeaf;
+            if (m3 > 0) {
+                for (const InvWs& w : ws) {
+                    const Sliced lr = rows_of(sliced_view(w.pl[slot], m, kLeaf), 2 * kLeaf, m3);
+                    g.push_back(update(w, lr, lr, m3, m3, r0 + 2 * kLeaf, r0 + 2 * kLeaf, true));
+                }
+                em.gemms(g);
+                g.clear();
+            }
+            em.record(evB(k));
+            em.on(0);
         }
+        // ---- diagonal block of k+1 (critical)
+        for (const InvWs& w : ws) {
+            const Sliced lp = sliced_view(w.pl[slot], m, kLeaf);
+            g.push_back(update(w, rows_of(lp, 0, nc), rows_of(lp, 0, nc), nc, nc, r0, r0, false));
+        }
+        em.gemms(g);
+        g.clear();
+    }
+    for (int s = 0; s < 2; ++s) {
+        if (!side_used[s]) continue;
+        em.on(s + 1);
+        em.record(evEnd0 + s);
+        em.on(0);
+        em.wait(evEnd0 + s);
     }
 }
 
@@ -1323,8 +1449,13 @@ extern "C" {
 int64_t pf_kernel_launch_count(void) { return g_launches.load(); }
 
 #ifdef PF_GEMM_PROBE
-int pf_gemm_probe_read(long long* out) {
-    return cudaMemcpyFromSymbol(out, pf::g_gemm_probe, sizeof(long long) * 16) == cudaSuccess ? 0 : 3;
+int pf_gemm_probe_read(long long* out) {  // 64 records of 8; returns the record count
+    int n = 0;
+    if (cudaMemcpyFromSymbol(out, pf::g_gemm_probe, sizeof(long long) * 64 * 16) != cudaSuccess) return -1;
+    if (cudaMemcpyFromSymbol(&n, pf::g_gemm_probe_n, sizeof(int)) != cudaSuccess) return -1;
+    const int zero = 0;
+    cudaMemcpyToSymbol(pf::g_gemm_probe_n, &zero, sizeof(int));
+    return n;
 }
 #endif
 

@@ -33,12 +33,29 @@
 namespace pf {
 
 #ifdef PF_GEMM_PROBE
-__device__ long long g_gemm_probe[16];
-#define PF_GSTAMP(i, cond)                                          \
-    do {                                                            \
-        if ((cond) && blockIdx.x == 0) g_gemm_probe[i] = clock64(); \
+// globaltimer stamps (ns) of CTA 0 of small beta != 0 GEMMs, one record of 8
+// per launch: [0..5] stamps, [6] rows, [7] cols
+__device__ long long g_gemm_probe[64 * 16];
+__device__ long long g_gemm_probe_epi[8];
+__device__ int g_gemm_probe_n;
+__device__ __forceinline__ long long gtimer() {
+    long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    return t;
+}
+#define PF_GSTAMP(i, cond)                                                      \
+    do {                                                                        \
+        if ((cond) && probe_on) reinterpret_cast<long long*>(tail + 128)[i] = gtimer(); \
+    } while (0)
+#define PF_ESTAMP(i)                                                                       \
+    do {                                                                                   \
+        if (blockIdx.x == 0 && threadIdx.x == 0 && P.beta != 0.0f && P.rows <= kTile && P.cols <= kTile) \
+            g_gemm_probe_epi[i] = gtimer();                                                \
     } while (0)
 #else
+#define PF_ESTAMP(i) \
+    do {             \
+    } while (0)
 #define PF_GSTAMP(i, cond) \
     do {                   \
     } while (0)
@@ -100,7 +117,11 @@ struct GemmTraits {
     static constexpr int kPlaneBytes = kFmt == kOZ8 ? 128 * 64 : 128 * 128;
     static constexpr int kStageBytes = 2 * kPlanes * kPlaneBytes;
     static constexpr int kStages = 3;
-    static constexpr int kSmemBytes = kStages * kStageBytes + 1024 + 256 + 4 * kTile;
+    // C-tile prefetch buffer (beta != 0, <= kStages-1 k-blocks): the unused
+    // last stage plus kCPad, rows padded to kCStride floats (bank rotation)
+    static constexpr int kCStride = kTile + 4;
+    static constexpr int kCPad = kFmt == kOZ8 ? kTile * kCStride * 4 - kStageBytes : 0;
+    static constexpr int kSmemBytes = kStages * kStageBytes + kCPad + 1024 + 256 + 4 * kTile;
     static constexpr int kKBlock = 64;  // elements per k-block (both formats)
     static constexpr int kKSteps = kFmt == kOZ8 ? 2 : 4;  // 32-byte UMMA k-steps per block
     static constexpr uint32_t kTmemCols = kFmt == kOZ8 ? 512 : 128;
@@ -156,40 +177,69 @@ __device__ __forceinline__ void decode_lower(int t, int& tm, int& tn) {
 // kernel (4 warps x 8 chunks) and the persistent inversion kernel (8 warps x
 // 4 chunks).  Global reads use ld.global.cg (data may come from other SMs of
 // the same persistent launch).
+// Per-row epilogue constants, loaded before the accumulator is ready.
+struct EpiRow {
+    float row_scale = 1.0f;
+    float diag_exact = 0.0f;
+};
+
+template <int kFmt>
+__device__ __forceinline__ EpiRow epi_row(const GemmDesc& P, int tm, int tn, int r) {
+    EpiRow e;
+    if constexpr (kFmt == kOZ8) {
+        if (r < P.rows) {
+            e.row_scale = P.alpha * ptx::pow2f(__ldcg(P.a_exp + r));
+            if ((P.flags & EPI_EXACT_DIAG) && tm == tn) e.diag_exact = static_cast<float>(__ldcg(P.a_sqnorm + r) * 0x1p14);
+        }
+    }
+    return e;
+}
+
 template <int kFmt>
 __device__ __forceinline__ void epilogue_chunks(const GemmDesc& P, int tm, int tn, uint32_t lane_base, int r,
                                                 const float* col_scale, int chunk_begin, int chunk_end,
-                                                bool have_acc) {
+                                                bool have_acc, const EpiRow& er, const float* crow = nullptr) {
     const bool row_ok = r < P.rows;
     const uint32_t f = P.flags;
     const bool mirror = (f & EPI_MIRROR) && tm != tn;
-    float row_scale = 1.0f;
+    const float row_scale = er.row_scale;
     const bool exact_diag = (f & EPI_EXACT_DIAG) && tm == tn && row_ok;
-    float diag_exact = 0.0f;
+    const float diag_exact = er.diag_exact;
+    PF_ESTAMP(0);
+    // kOZ8: the four digit accumulators of chunk c+1 are loaded from TMEM while
+    // chunk c is recombined and stored
+    uint32_t raw[kFmt == kOZ8 ? kDigits : 1][16];
     if constexpr (kFmt == kOZ8) {
-        if (row_ok) row_scale = P.alpha * ptx::pow2f(__ldcg(P.a_exp + r));
-        if (exact_diag) diag_exact = static_cast<float>(__ldcg(P.a_sqnorm + r) * 0x1p14);
+        if (have_acc) {
+            __syncwarp();
+#pragma unroll
+            for (int g = 0; g < kDigits; ++g) ptx::tmem_ld16_nowait(lane_base + g * 128 + chunk_begin * 16, raw[g]);
+#pragma unroll
+            for (int g = 0; g < kDigits; ++g) ptx::tmem_wait_ld_dep(raw[g]);
+        } else {
+#pragma unroll
+            for (int g = 0; g < kDigits; ++g)
+#pragma unroll
+                for (int j = 0; j < 16; ++j) raw[g][j] = 0u;
+        }
+        PF_ESTAMP(1);
     }
 #pragma unroll 1
     for (int chunk = chunk_begin; chunk < chunk_end; ++chunk) {
         __syncwarp();  // tcgen05.ld is .sync.aligned: re-converge first
         const int c0 = tn * kTile + chunk * 16;
         float out[16];
+        [[maybe_unused]] uint32_t nxt[kFmt == kOZ8 ? kDigits : 1][16];
+        [[maybe_unused]] const bool more = have_acc && chunk + 1 < chunk_end;
         if constexpr (kFmt == kOZ8) {
+            if (more) {
+#pragma unroll
+                for (int g = 0; g < kDigits; ++g)
+                    ptx::tmem_ld16_nowait(lane_base + g * 128 + (chunk + 1) * 16, nxt[g]);
+            }
             // accumulator g counts units of 2^-7(g+2) of 2^(e_a + e_b); the four
             // exact int32 sums are recombined smallest-first in fp32 (the result
             // is stored in fp32: ~1 ulp, no accumulation error)
-            uint32_t raw[kDigits][16];
-            if (have_acc) {
-#pragma unroll
-                for (int g = 0; g < kDigits; ++g) ptx::tmem_ld16_nowait(lane_base + g * 128 + chunk * 16, raw[g]);
-                ptx::tmem_wait_ld();
-            } else {
-#pragma unroll
-                for (int g = 0; g < kDigits; ++g)
-#pragma unroll
-                    for (int j = 0; j < 16; ++j) raw[g][j] = 0u;
-            }
             const bool diag_chunk = exact_diag && r >= c0 && r < c0 + 16;
 #pragma unroll
             for (int j = 0; j < 16; ++j) {
@@ -212,57 +262,85 @@ __device__ __forceinline__ void epilogue_chunks(const GemmDesc& P, int tm, int t
 #pragma unroll
             for (int j = 0; j < 16; ++j) out[j] = P.alpha * v[j];
         }
-        if (!row_ok || c0 >= P.cols) continue;
-        const bool full_chunk = c0 + 16 <= P.cols;
-        if (P.beta != 0.0f) {
-            float cv[16];
-            if ((f & EPI_VEC4) && full_chunk && !(f & EPI_TRANSPOSE)) {
-                const float4* src = reinterpret_cast<const float4*>(P.c + static_cast<size_t>(r) * P.ldc + c0);  // read via ld.cg below
+        if (row_ok && c0 < P.cols) {
+            const bool full_chunk = c0 + 16 <= P.cols;
+            if (P.beta != 0.0f) {
+                float cv[16];
+                if (crow && full_chunk) {  // C row prefetched into shared memory
+                    const float4* src = reinterpret_cast<const float4*>(crow + chunk * 16);
 #pragma unroll
-                for (int q = 0; q < 4; ++q) {
-                    const float4 t = __ldcg(src + q);
-                    cv[4 * q] = t.x;
-                    cv[4 * q + 1] = t.y;
-                    cv[4 * q + 2] = t.z;
-                    cv[4 * q + 3] = t.w;
+                    for (int q = 0; q < 4; ++q) {
+                        const float4 t = src[q];
+                        cv[4 * q] = t.x;
+                        cv[4 * q + 1] = t.y;
+                        cv[4 * q + 2] = t.z;
+                        cv[4 * q + 3] = t.w;
+                    }
+                } else if ((f & EPI_VEC4) && full_chunk && !(f & EPI_TRANSPOSE)) {
+                    const float4* src = reinterpret_cast<const float4*>(P.c + static_cast<size_t>(r) * P.ldc + c0);  // read via ld.cg below
+#pragma unroll
+                    for (int q = 0; q < 4; ++q) {
+                        const float4 t = __ldcg(src + q);
+                        cv[4 * q] = t.x;
+                        cv[4 * q + 1] = t.y;
+                        cv[4 * q + 2] = t.z;
+                        cv[4 * q + 3] = t.w;
+                    }
+                } else {
+#pragma unroll
+                    for (int j = 0; j < 16; ++j) {
+                        const int c = c0 + j;
+                        const size_t idx = (f & EPI_TRANSPOSE) ? static_cast<size_t>(c) * P.ldc + r
+                                                               : static_cast<size_t>(r) * P.ldc + c;
+                        cv[j] = c < P.cols ? __ldcg(P.c + idx) : 0.0f;
+                    }
                 }
+#pragma unroll
+                for (int j = 0; j < 16; ++j) out[j] = fmaf(P.beta, cv[j], out[j]);
+            }
+#ifdef PF_PROBE_NOSTORE
+            if (P.beta != 0.0f && P.rows <= kTile && P.cols <= kTile) {
+                if (out[0] == 12345.678f) P.c[0] = out[1];  // keep the values live
+            } else
+#endif
+            if ((f & EPI_VEC4) && full_chunk && !(f & EPI_TRANSPOSE)) {
+                float4* dst = reinterpret_cast<float4*>(P.c + static_cast<size_t>(r) * P.ldc + c0);
+#pragma unroll
+                for (int q = 0; q < 4; ++q)
+                    dst[q] = make_float4(out[4 * q], out[4 * q + 1], out[4 * q + 2], out[4 * q + 3]);
+            } else if (f & EPI_TRANSPOSE) {
+                // lanes hold consecutive rows -> each transposed column store is coalesced
+#pragma unroll
+                for (int j = 0; j < 16; ++j)
+                    if (c0 + j < P.cols) P.c[static_cast<size_t>(c0 + j) * P.ldc + r] = out[j];
             } else {
 #pragma unroll
-                for (int j = 0; j < 16; ++j) {
-                    const int c = c0 + j;
-                    const size_t idx = (f & EPI_TRANSPOSE) ? static_cast<size_t>(c) * P.ldc + r
-                                                           : static_cast<size_t>(r) * P.ldc + c;
-                    cv[j] = c < P.cols ? __ldcg(P.c + idx) : 0.0f;
-                }
+                for (int j = 0; j < 16; ++j)
+                    if (c0 + j < P.cols) P.c[static_cast<size_t>(r) * P.ldc + c0 + j] = out[j];
             }
+            if (mirror) {
 #pragma unroll
-            for (int j = 0; j < 16; ++j) out[j] = fmaf(P.beta, cv[j], out[j]);
+                for (int j = 0; j < 16; ++j)
+                    if (c0 + j < P.cols) P.c[static_cast<size_t>(c0 + j) * P.ldc + r] = out[j];
+            }
+            if (f & EPI_ALSO_T) {
+#pragma unroll
+                for (int j = 0; j < 16; ++j)
+                    if (c0 + j < P.cols) P.c_t[static_cast<size_t>(c0 + j) * P.ldc_t + r] = out[j];
+            }
         }
-        if ((f & EPI_VEC4) && full_chunk && !(f & EPI_TRANSPOSE)) {
-            float4* dst = reinterpret_cast<float4*>(P.c + static_cast<size_t>(r) * P.ldc + c0);
+        if constexpr (kFmt == kOZ8) {
+            if (more) {
+                __syncwarp();
 #pragma unroll
-            for (int q = 0; q < 4; ++q)
-                dst[q] = make_float4(out[4 * q], out[4 * q + 1], out[4 * q + 2], out[4 * q + 3]);
-        } else if (f & EPI_TRANSPOSE) {
-            // lanes hold consecutive rows -> each transposed column store is coalesced
+                for (int g = 0; g < kDigits; ++g) ptx::tmem_wait_ld_dep(nxt[g]);
 #pragma unroll
-            for (int j = 0; j < 16; ++j)
-                if (c0 + j < P.cols) P.c[static_cast<size_t>(c0 + j) * P.ldc + r] = out[j];
-        } else {
+                for (int g = 0; g < kDigits; ++g)
 #pragma unroll
-            for (int j = 0; j < 16; ++j)
-                if (c0 + j < P.cols) P.c[static_cast<size_t>(r) * P.ldc + c0 + j] = out[j];
+                    for (int jj = 0; jj < 16; ++jj) raw[g][jj] = nxt[g][jj];
+            }
         }
-        if (mirror) {
-#pragma unroll
-            for (int j = 0; j < 16; ++j)
-                if (c0 + j < P.cols) P.c[static_cast<size_t>(c0 + j) * P.ldc + r] = out[j];
-        }
-        if (f & EPI_ALSO_T) {
-#pragma unroll
-            for (int j = 0; j < 16; ++j)
-                if (c0 + j < P.cols) P.c_t[static_cast<size_t>(c0 + j) * P.ldc_t + r] = out[j];
-        }
+        if (chunk - chunk_begin < 4) PF_ESTAMP(2 + chunk - chunk_begin);
     }
 
 }
@@ -275,11 +353,13 @@ __global__ void __launch_bounds__(GemmTraits<kFmt>::kThreads, GemmTraits<kFmt>::
     extern __shared__ uint8_t smem_raw[];
     uint8_t* smem = reinterpret_cast<uint8_t*>(
         (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~static_cast<uintptr_t>(1023));
-    uint64_t* full = reinterpret_cast<uint64_t*>(smem + kStages * T::kStageBytes);
+    uint8_t* tail = smem + kStages * T::kStageBytes + T::kCPad;
+    uint64_t* full = reinterpret_cast<uint64_t*>(tail);
     uint64_t* empty = full + kStages;
     uint64_t* done = empty + kStages;
-    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(done + 1);
-    float* col_scale = reinterpret_cast<float*>(smem + kStages * T::kStageBytes + 256);  // kOZ8: 2^e_b per tile column
+    uint64_t* cbar = done + 1;
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(cbar + 1);
+    float* col_scale = reinterpret_cast<float*>(tail + 256);  // kOZ8: 2^e_b per tile column
 
     const int gt = blockIdx.x;
     int p = 0, lt;
@@ -303,7 +383,15 @@ __global__ void __launch_bounds__(GemmTraits<kFmt>::kThreads, GemmTraits<kFmt>::
 
     const int warp = threadIdx.x >> 5;
     const uint32_t lane = threadIdx.x & 31;
+    // short-K beta != 0 tiles read C into the idle last stage while the MMAs run
+    const int c_cols = min(kTile, P.cols - tn * kTile);
+    const bool cpre = kFmt == kOZ8 && P.beta != 0.0f && kb1 - kb0 <= kStages - 1 && (P.flags & EPI_VEC4) &&
+                      !(P.flags & EPI_TRANSPOSE) && c_cols > 0 && (c_cols & 3) == 0;
+    float* cbuf = reinterpret_cast<float*>(smem + (kStages - 1) * T::kStageBytes);
 
+#ifdef PF_GEMM_PROBE
+    const bool probe_on = blockIdx.x == 0 && P.beta != 0.0f && P.rows <= kTile && P.cols <= kTile;
+#endif
     PF_GSTAMP(0, threadIdx.x == 0);
     // prologue (overlaps the previous kernel's tail under PDL)
     if (threadIdx.x == 0) {
@@ -312,6 +400,7 @@ __global__ void __launch_bounds__(GemmTraits<kFmt>::kThreads, GemmTraits<kFmt>::
             ptx::mbar_init(&empty[s], 1);
         }
         ptx::mbar_init(done, 1);
+        ptx::mbar_init(cbar, kTile);
         ptx::fence_barrier_init();
     }
     if (warp == 0) ptx::tmem_alloc<T::kTmemCols>(tmem_slot);
@@ -325,6 +414,17 @@ __global__ void __launch_bounds__(GemmTraits<kFmt>::kThreads, GemmTraits<kFmt>::
     ptx::tc_fence_after();
     const uint32_t tmem = *tmem_slot;
     PF_GSTAMP(1, threadIdx.x == 0);
+    if (cpre && threadIdx.x >= 64 && threadIdx.x < 64 + kTile) {  // warps 2-5: one C row each
+        const int t = static_cast<int>(threadIdx.x) - 64;
+        const int r = tm * kTile + t;
+        if (r < P.rows) {
+            const uint32_t bytes = static_cast<uint32_t>(c_cols) * 4u;
+            ptx::mbar_arrive_expect_tx(cbar, bytes);
+            ptx::bulk_load(cbuf + t * T::kCStride, P.c + static_cast<size_t>(r) * P.ldc + tn * kTile, bytes, cbar);
+        } else {
+            ptx::mbar_arrive(cbar);
+        }
+    }
 
     auto a_plane = [&](int s, int pl) { return smem + s * T::kStageBytes + pl * T::kPlaneBytes; };
     auto b_plane = [&](int s, int pl) {
@@ -402,6 +502,7 @@ __global__ void __launch_bounds__(GemmTraits<kFmt>::kThreads, GemmTraits<kFmt>::
     }
 
     // ---------------- epilogue: TMEM -> registers -> global
+    const EpiRow er = epi_row<kFmt>(P, tm, tn, tm * kTile + (warp & 3) * 32 + static_cast<int>(lane));
     const bool have_acc = kb1 > kb0;
     if (have_acc) {
         ptx::mbar_wait(done, 0);
@@ -409,6 +510,7 @@ __global__ void __launch_bounds__(GemmTraits<kFmt>::kThreads, GemmTraits<kFmt>::
     }
     PF_GSTAMP(4, threadIdx.x == 0);
     ptx::grid_dep_launch();  // main loop done: let the next launch start its prologue
+    if (cpre) ptx::mbar_wait(cbar, 0);
     __syncwarp();
     {
         constexpr int kPairs = T::kThreads / 128;  // warps sharing a TMEM lane quarter
@@ -416,12 +518,25 @@ __global__ void __launch_bounds__(GemmTraits<kFmt>::kThreads, GemmTraits<kFmt>::
         constexpr int kChunks = kTile / 16 / kPairs;
         epilogue_chunks<kFmt>(P, tm, tn, tmem + (static_cast<uint32_t>(ew * 32) << 16),
                               tm * kTile + ew * 32 + static_cast<int>(lane), col_scale, part * kChunks,
-                              (part + 1) * kChunks, have_acc);
+                              (part + 1) * kChunks, have_acc, er,
+                              cpre ? cbuf + (ew * 32 + static_cast<int>(lane)) * T::kCStride : nullptr);
     }
 
     PF_GSTAMP(5, threadIdx.x == 0);
     ptx::tc_fence_before();
     __syncthreads();
+#ifdef PF_GEMM_PROBE
+    if (probe_on && threadIdx.x == 0) {
+        const int slot = atomicAdd(&g_gemm_probe_n, 1);
+        if (slot < 64) {
+            const long long* st = reinterpret_cast<const long long*>(tail + 128);
+            for (int i = 0; i < 6; ++i) g_gemm_probe[slot * 16 + i] = st[i];
+            for (int i = 0; i < 8; ++i) g_gemm_probe[slot * 16 + 6 + i] = g_gemm_probe_epi[i];
+            g_gemm_probe[slot * 16 + 14] = P.rows;
+            g_gemm_probe[slot * 16 + 15] = P.cols;
+        }
+    }
+#endif
     if (warp == 0) ptx::tmem_dealloc<T::kTmemCols>(tmem);
 }
 
