@@ -213,15 +213,21 @@ void launch_slices(const std::vector<SliceReq>& reqs, cudaStream_t st) {
     for (std::size_t i = 0; i < reqs.size(); i += kMaxSliceJobs) {
         SliceBatch b{};
         const int cnt = static_cast<int>(std::min<std::size_t>(kMaxSliceJobs, reqs.size() - i));
-        int rows = 1;
+        int rows = 1, kmax = 0;
         for (int j = 0; j < cnt; ++j) {
             const SliceReq& r = reqs[i + j];
             b.j[j] = SliceJob{r.src, r.dst.rows, r.dst.k, r.ld, r.mode, r.dst.planes,
                               r.dst.plane_stride, r.dst.kpad, r.dst.exps, r.dst.sqnorm};
             rows = std::max(rows, r.dst.rows);
+            kmax = std::max(kmax, r.dst.k);
         }
-        launch(slice_kernel, dim3((rows + 7) / 8, cnt), dim3(256), 0, st, b);
-        after_launch("slice_kernel");
+        if (kmax > 1024 && kmax <= 4 * kLongThreads * kLongVec) {  // block per row, one pass
+            launch(slice_long_kernel, dim3(rows, cnt), dim3(kLongThreads), 0, st, b);
+            after_launch("slice_long_kernel");
+        } else {
+            launch(slice_kernel, dim3((rows + 7) / 8, cnt), dim3(256), 0, st, b);
+            after_launch("slice_kernel");
+        }
     }
 }
 

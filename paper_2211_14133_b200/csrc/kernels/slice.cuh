@@ -52,22 +52,62 @@ __device__ __forceinline__ void valid_range(const SliceJob& J, int r, int& lo, i
     if (J.mode == SLICE_UPPER_BLOCK) lo = (r / 128) * 128;
 }
 
-__device__ __forceinline__ void slice_digits(float x, int e, int8_t (&q)[4], double& rep) {
-    float t = ldexpf(x, 7 - e);  // x * 2^-e * 2^7, |t| < 128 (exact: power-of-two scaling)
-    const float q0 = truncf(t);
-    t = (t - q0) * 128.0f;
-    const float q1 = truncf(t);
-    t = (t - q1) * 128.0f;
-    const float q2 = truncf(t);
-    t = (t - q2) * 128.0f;
-    const float q3 = fminf(fmaxf(rintf(t), -127.0f), 127.0f);
-    q[0] = static_cast<int8_t>(q0);
-    q[1] = static_cast<int8_t>(q1);
-    q[2] = static_cast<int8_t>(q2);
-    q[3] = static_cast<int8_t>(q3);
-    rep = static_cast<double>(q0) * 0x1p-7 + static_cast<double>(q1) * 0x1p-14 +
-          static_cast<double>(q2) * 0x1p-21 + static_cast<double>(q3) * 0x1p-28;
+// Row scale 2^(28-e) as one exact multiplier (0 = out of the normal range:
+// fall back to ldexpf per element).
+__device__ __forceinline__ float digit_scale(int e) {
+    const int k = 28 - e;
+    return (k >= -126 && k <= 127) ? __int_as_float((k + 127) << 23) : 0.0f;
 }
+
+// Digits of x (row exponent e, sc = digit_scale(e)), in integer arithmetic:
+// A = |x| 2^(28-e) < 2^28 (exact scaling); with I = trunc(A), R = rint(A)
+//   q0 = I >> 21, q1 = (I >> 14) & 127, q2 = (I >> 7) & 127,
+//   q3 = min(R - (I & ~127), 127),   all carrying the sign of x
+// -- the same digits as truncating t = x 2^(7-e) digit by digit and rounding
+// the last (ties-to-even parity of R equals that of t's last digit), with two
+// float->int conversions instead of eight.  Returns |Q| = |x~| 2^(28-e).
+__device__ __forceinline__ int slice_digits(float x, int e, float sc, int8_t (&q)[4]) {
+    const float a = fabsf(sc != 0.0f ? x * sc : ldexpf(x, 28 - e));
+    const int I = __float2int_rz(a);
+    const int R = __float2int_rn(a);
+    const int hi = I & ~127;
+    const int d3 = min(R - hi, 127);
+    const int neg = x < 0.0f ? -1 : 0;
+    q[0] = static_cast<int8_t>(((I >> 21) ^ neg) - neg);
+    q[1] = static_cast<int8_t>((((I >> 14) & 127) ^ neg) - neg);
+    q[2] = static_cast<int8_t>((((I >> 7) & 127) ^ neg) - neg);
+    q[3] = static_cast<int8_t>((d3 ^ neg) - neg);
+    return hi + d3;
+}
+
+// Exact sum of Q^2 (< 2^69 for rows up to 8192): 128-bit integer, so the
+// squared norm is independent of the summation order (every kernel that
+// slices a row -- warp, block or persistent task -- writes the same bits).
+struct SqAcc {
+    unsigned long long lo = 0, hi = 0;
+    __device__ __forceinline__ void add(int qv) {
+        const unsigned long long v = static_cast<unsigned long long>(static_cast<long long>(qv) * qv);
+        lo += v;
+        hi += lo < v ? 1ull : 0ull;
+    }
+    __device__ __forceinline__ void add(const SqAcc& o) {
+        lo += o.lo;
+        hi += o.hi + (lo < o.lo ? 1ull : 0ull);
+    }
+    __device__ __forceinline__ void warp_reduce() {
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+            SqAcc t;
+            t.lo = __shfl_xor_sync(0xffffffffu, lo, o);
+            t.hi = __shfl_xor_sync(0xffffffffu, hi, o);
+            add(t);
+        }
+    }
+    // sum x~^2 2^-2e = sum Q^2 2^-56
+    __device__ __forceinline__ double value() const {
+        return (static_cast<double>(hi) * 0x1p64 + static_cast<double>(lo)) * 0x1p-56;
+    }
+};
 
 // One warp slices row r of job J.  Rows whose valid range is 16-byte aligned
 // move 4 elements per lane per access (float4 in, char4 out) with 4 accesses
@@ -97,7 +137,8 @@ __device__ __forceinline__ void slice_row(const SliceJob& J, int r, int lane) {
         int e = 0;
         if (m > 0.0f) frexpf(m, &e);
         if (lane == 0) J.exps[r] = e;
-        double sq = 0.0;
+        const float sc = digit_scale(e);
+        SqAcc sq;
 #pragma unroll
         for (int u = 0; u < 8; ++u) {
             const int c = lane + 32 * u;
@@ -107,9 +148,7 @@ __device__ __forceinline__ void slice_row(const SliceJob& J, int r, int lane) {
 #pragma unroll
             for (int w = 0; w < 4; ++w) {
                 int8_t q[4];
-                double rep;
-                slice_digits(xs[w], e, q, rep);
-                sq = fma(rep, rep, sq);
+                sq.add(slice_digits(xs[w], e, sc, q));
 #pragma unroll
                 for (int pl = 0; pl < 4; ++pl)
                     packed[pl] |= static_cast<uint32_t>(static_cast<uint8_t>(q[pl])) << (8 * w);
@@ -119,8 +158,8 @@ __device__ __forceinline__ void slice_row(const SliceJob& J, int r, int lane) {
                 *reinterpret_cast<uint32_t*>(p0 + lo + 4 * c + pl * J.plane_stride) = packed[pl];
         }
 #pragma unroll
-        for (int o = 16; o > 0; o >>= 1) sq += __shfl_xor_sync(0xffffffffu, sq, o);
-        if (lane == 0) J.sqnorm[r] = sq;
+        sq.warp_reduce();
+        if (lane == 0) J.sqnorm[r] = sq.value();
         return;
     }
     if (vec) {
@@ -151,7 +190,8 @@ __device__ __forceinline__ void slice_row(const SliceJob& J, int r, int lane) {
         e = ex;          // so max|row| < 2^e
     }
     if (lane == 0) J.exps[r] = e;
-    double sq = 0.0;
+    const float sc = digit_scale(e);
+    SqAcc sq;
     if (vec) {
         const float4* r4 = reinterpret_cast<const float4*>(row + lo);
         const int n4 = (hi - lo) / 4;
@@ -162,9 +202,7 @@ __device__ __forceinline__ void slice_row(const SliceJob& J, int r, int lane) {
 #pragma unroll
             for (int u = 0; u < 4; ++u) {
                 int8_t q[4];
-                double rep;
-                slice_digits(xs[u], e, q, rep);
-                sq = fma(rep, rep, sq);
+                sq.add(slice_digits(xs[u], e, sc, q));
 #pragma unroll
                 for (int pl = 0; pl < 4; ++pl)
                     packed[pl] |= static_cast<uint32_t>(static_cast<uint8_t>(q[pl])) << (8 * u);
@@ -176,16 +214,94 @@ __device__ __forceinline__ void slice_row(const SliceJob& J, int r, int lane) {
     } else {
         for (int c = lo + lane; c < hi; c += 32) {
             int8_t q[4];
-            double rep;
-            slice_digits(__ldcg(row + c), e, q, rep);
-            sq = fma(rep, rep, sq);
+            sq.add(slice_digits(__ldcg(row + c), e, sc, q));
 #pragma unroll
             for (int pl = 0; pl < 4; ++pl) p0[c + pl * J.plane_stride] = q[pl];
         }
     }
+    sq.warp_reduce();
+    if (lane == 0) J.sqnorm[r] = sq.value();
+}
+
+// Long rows (1024 < valid length <= 8192, 16-byte aligned): one 256-thread
+// block per row, each thread holding up to 8 float4 in registers, so the row
+// is read from global memory ONCE with 8 loads in flight per thread (the
+// warp-per-row path above reads long rows twice with one load in flight).
+constexpr int kLongThreads = 256;
+constexpr int kLongVec = 8;  // float4 per thread -> rows up to 8192
+
+__device__ __forceinline__ bool long_row_ok(const SliceJob& J, int r, int& lo, int& hi) {
+    valid_range(J, r, lo, hi);
+    const float* row = J.src + static_cast<int64_t>(r) * J.ld;
+    int8_t* p0 = J.planes + static_cast<int64_t>(r) * J.kpad;
+    return ((reinterpret_cast<uintptr_t>(row + lo) & 15) == 0) && ((hi - lo) % 4 == 0) &&
+           ((reinterpret_cast<uintptr_t>(p0 + lo) & 3) == 0) && (J.plane_stride % 4 == 0) &&
+           hi - lo <= 4 * kLongThreads * kLongVec;
+}
+
+__global__ void __launch_bounds__(kLongThreads) slice_long_kernel(const __grid_constant__ SliceBatch b) {
+    const SliceJob& J = b.j[blockIdx.y];
+    const int r = blockIdx.x;
+    ptx::grid_dep_wait();
+    ptx::grid_dep_launch();
+    if (r >= J.rows) return;
+    const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
+    int lo, hi;
+    if (!long_row_ok(J, r, lo, hi)) {  // unaligned / over-long rows: warp path
+        if (warp == 0) slice_row(J, r, lane);
+        return;
+    }
+    __shared__ float red_m[kLongThreads / 32];
+    __shared__ SqAcc red_s[kLongThreads / 32];
+    const float4* r4 = reinterpret_cast<const float4*>(J.src + static_cast<int64_t>(r) * J.ld + lo);
+    int8_t* p0 = J.planes + static_cast<int64_t>(r) * J.kpad + lo;
+    const int n4 = (hi - lo) / 4;
+    float4 v[kLongVec];
 #pragma unroll
-    for (int o = 16; o > 0; o >>= 1) sq += __shfl_xor_sync(0xffffffffu, sq, o);
-    if (lane == 0) J.sqnorm[r] = sq;
+    for (int u = 0; u < kLongVec; ++u)
+        v[u] = (t + kLongThreads * u < n4) ? __ldcg(r4 + t + kLongThreads * u) : make_float4(0.f, 0.f, 0.f, 0.f);
+    float m = 0.0f;
+#pragma unroll
+    for (int u = 0; u < kLongVec; ++u)
+        m = fmaxf(m, fmaxf(fmaxf(fabsf(v[u].x), fabsf(v[u].y)), fmaxf(fabsf(v[u].z), fabsf(v[u].w))));
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, o));
+    if (lane == 0) red_m[warp] = m;
+    __syncthreads();
+    m = red_m[0];
+#pragma unroll
+    for (int w = 1; w < kLongThreads / 32; ++w) m = fmaxf(m, red_m[w]);
+    int e = 0;
+    if (m > 0.0f) frexpf(m, &e);
+    if (t == 0) J.exps[r] = e;
+    const float sc = digit_scale(e);
+    SqAcc sq;
+#pragma unroll
+    for (int u = 0; u < kLongVec; ++u) {
+        const int c = t + kLongThreads * u;
+        if (c >= n4) continue;
+        const float xs[4] = {v[u].x, v[u].y, v[u].z, v[u].w};
+        uint32_t packed[4] = {0u, 0u, 0u, 0u};
+#pragma unroll
+        for (int w = 0; w < 4; ++w) {
+            int8_t q[4];
+            sq.add(slice_digits(xs[w], e, sc, q));
+#pragma unroll
+            for (int pl = 0; pl < 4; ++pl)
+                packed[pl] |= static_cast<uint32_t>(static_cast<uint8_t>(q[pl])) << (8 * w);
+        }
+#pragma unroll
+        for (int pl = 0; pl < 4; ++pl) *reinterpret_cast<uint32_t*>(p0 + 4 * c + pl * J.plane_stride) = packed[pl];
+    }
+    sq.warp_reduce();
+    if (lane == 0) red_s[warp] = sq;
+    __syncthreads();
+    if (t == 0) {
+        SqAcc tot;
+#pragma unroll
+        for (int w = 0; w < kLongThreads / 32; ++w) tot.add(red_s[w]);
+        J.sqnorm[r] = tot.value();
+    }
 }
 
 // one warp per row; grid (ceil(rows / 8), jobs)

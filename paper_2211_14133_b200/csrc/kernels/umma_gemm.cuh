@@ -206,37 +206,27 @@ __device__ __forceinline__ void epilogue_chunks(const GemmDesc& P, int tm, int t
     const bool exact_diag = (f & EPI_EXACT_DIAG) && tm == tn && row_ok;
     const float diag_exact = er.diag_exact;
     PF_ESTAMP(0);
-    // kOZ8: the four digit accumulators of chunk c+1 are loaded from TMEM while
-    // chunk c is recombined and stored
-    uint32_t raw[kFmt == kOZ8 ? kDigits : 1][16];
-    if constexpr (kFmt == kOZ8) {
-        if (have_acc) {
-            __syncwarp();
-#pragma unroll
-            for (int g = 0; g < kDigits; ++g) ptx::tmem_ld16_nowait(lane_base + g * 128 + chunk_begin * 16, raw[g]);
-#pragma unroll
-            for (int g = 0; g < kDigits; ++g) ptx::tmem_wait_ld_dep(raw[g]);
-        } else {
-#pragma unroll
-            for (int g = 0; g < kDigits; ++g)
-#pragma unroll
-                for (int j = 0; j < 16; ++j) raw[g][j] = 0u;
-        }
-        PF_ESTAMP(1);
-    }
 #pragma unroll 1
     for (int chunk = chunk_begin; chunk < chunk_end; ++chunk) {
         __syncwarp();  // tcgen05.ld is .sync.aligned: re-converge first
         const int c0 = tn * kTile + chunk * 16;
         float out[16];
-        [[maybe_unused]] uint32_t nxt[kFmt == kOZ8 ? kDigits : 1][16];
-        [[maybe_unused]] const bool more = have_acc && chunk + 1 < chunk_end;
         if constexpr (kFmt == kOZ8) {
-            if (more) {
+            // TMEM reads (64 B/clk per SM) bound this epilogue: 4 accumulators
+            // x 64 KB per tile
+            uint32_t raw[kDigits][16];
+            if (have_acc) {
+#pragma unroll
+                for (int g = 0; g < kDigits; ++g) ptx::tmem_ld16_nowait(lane_base + g * 128 + chunk * 16, raw[g]);
+#pragma unroll
+                for (int g = 0; g < kDigits; ++g) ptx::tmem_wait_ld_dep(raw[g]);
+            } else {
 #pragma unroll
                 for (int g = 0; g < kDigits; ++g)
-                    ptx::tmem_ld16_nowait(lane_base + g * 128 + (chunk + 1) * 16, nxt[g]);
+#pragma unroll
+                    for (int j = 0; j < 16; ++j) raw[g][j] = 0u;
             }
+            if (chunk == chunk_begin) PF_ESTAMP(1);
             // accumulator g counts units of 2^-7(g+2) of 2^(e_a + e_b); the four
             // exact int32 sums are recombined smallest-first in fp32 (the result
             // is stored in fp32: ~1 ulp, no accumulation error)
@@ -327,17 +317,6 @@ __device__ __forceinline__ void epilogue_chunks(const GemmDesc& P, int tm, int t
 #pragma unroll
                 for (int j = 0; j < 16; ++j)
                     if (c0 + j < P.cols) P.c_t[static_cast<size_t>(c0 + j) * P.ldc_t + r] = out[j];
-            }
-        }
-        if constexpr (kFmt == kOZ8) {
-            if (more) {
-                __syncwarp();
-#pragma unroll
-                for (int g = 0; g < kDigits; ++g) ptx::tmem_wait_ld_dep(nxt[g]);
-#pragma unroll
-                for (int g = 0; g < kDigits; ++g)
-#pragma unroll
-                    for (int jj = 0; jj < 16; ++jj) raw[g][jj] = nxt[g][jj];
             }
         }
         if (chunk - chunk_begin < 4) PF_ESTAMP(2 + chunk - chunk_begin);
