@@ -151,12 +151,13 @@ void encode(CUtensorMap* m, const void* ptr, bool bf16, int rows, int k, size_t 
 
 // 3-D map over the 4 digit planes of a sliced operand: dims {k, rows, plane},
 // box {64, 128, 4} (one TMA per operand tile per k-block).
-void encode_planes(CUtensorMap* m, const int8_t* planes, int rows, int k, int kpad, int64_t plane_stride) {
+void encode_planes(CUtensorMap* m, const int8_t* planes, int rows, int k, int kpad, int64_t plane_stride,
+                   int box_rows = 128) {
     if (!aligned16(planes) || kpad % 16 != 0 || plane_stride % 16 != 0)
         throw std::invalid_argument("digit planes need 16-byte aligned rows and planes");
     const cuuint64_t dims[3] = {static_cast<cuuint64_t>(k), static_cast<cuuint64_t>(rows), 4};
     const cuuint64_t strides[2] = {static_cast<cuuint64_t>(kpad), static_cast<cuuint64_t>(plane_stride)};
-    const cuuint32_t box[3] = {64, 128, 4};
+    const cuuint32_t box[3] = {64, static_cast<cuuint32_t>(box_rows), 4};
     const cuuint32_t estr[3] = {1, 1, 1};
     const CUresult r = encoder()(m, CU_TENSOR_MAP_DATA_TYPE_UINT8, 3, const_cast<int8_t*>(planes), dims, strides,
                                  box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_64B,
@@ -251,9 +252,9 @@ struct GemmSpec {
 
 // GemmSpec -> GemmDesc, encoding its operand tensor maps at maps[*n_maps...]
 // (tile_begin left to the caller).  Returns the number of maps used.
-template <int kFmt>
+template <int kFmt, int kN = 128>
 int make_desc(const GemmSpec& s, GemmDesc& d, CUtensorMap* maps, int n_maps) {
-    using T = GemmTraits<kFmt>;
+    using T = GemmTraits<kFmt, kN>;
     const bool shared_ab = kFmt == kBF16 ? (s.a_bf16 == s.b_bf16 && s.lda == s.ldb) : (s.a.planes == s.b.planes);
     int m = n_maps;
     auto put_maps = [&](bool is_a) {
@@ -263,19 +264,19 @@ int make_desc(const GemmSpec& s, GemmDesc& d, CUtensorMap* maps, int n_maps) {
                    static_cast<size_t>(is_a ? s.lda : s.ldb) * 2);
         } else {
             const Sliced& o = is_a ? s.a : s.b;
-            encode_planes(&maps[m++], o.planes, o.rows, o.k, o.kpad, o.plane_stride);
+            encode_planes(&maps[m++], o.planes, o.rows, o.k, o.kpad, o.plane_stride, is_a ? kTile : kN);
         }
         return first;
     };
     std::memset(&d, 0, sizeof(d));
     d.a_map = put_maps(true);
-    d.b_map = shared_ab ? d.a_map : put_maps(false);
+    d.b_map = shared_ab && kN == kTile ? d.a_map : put_maps(false);  // B box is kN rows
     if (kFmt == kOZ8 && shared_ab) d.flags |= EPI_EXACT_DIAG;
     d.rows = s.rows;
     d.cols = s.cols;
     d.k = s.k;
     d.tiles_m = (s.rows + kTile - 1) / kTile;
-    d.tiles_n = (s.cols + kTile - 1) / kTile;
+    d.tiles_n = (s.cols + kN - 1) / kN;
     d.lower = s.lower ? 1 : 0;
     d.k_mode = s.k_mode;
     d.alpha = s.alpha;
@@ -294,10 +295,10 @@ int make_desc(const GemmSpec& s, GemmDesc& d, CUtensorMap* maps, int n_maps) {
 
 inline int desc_tiles(const GemmDesc& d) { return d.lower ? d.tiles_m * (d.tiles_m + 1) / 2 : d.tiles_m * d.tiles_n; }
 
-template <int kFmt>
-void launch_gemms(const std::vector<GemmSpec>& specs, cudaStream_t stream) {
-    using T = GemmTraits<kFmt>;
-    auto kernel = umma_gemm_kernel<kFmt>;
+template <int kFmt, int kN>
+void launch_gemms_n(const std::vector<GemmSpec>& specs, cudaStream_t stream) {
+    using T = GemmTraits<kFmt, kN>;
+    auto kernel = umma_gemm_kernel<kFmt, kN>;
     static std::once_flag attr_once;
     std::call_once(attr_once, [&] {
         check(cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, T::kSmemBytes),
@@ -311,7 +312,7 @@ void launch_gemms(const std::vector<GemmSpec>& specs, cudaStream_t stream) {
         while (i < specs.size() && probs < kMaxProbs) {
             if (maps + 2 > kMaxMaps) break;
             GemmDesc& d = batch.probs[probs];
-            maps += make_desc<kFmt>(specs[i], d, batch.maps, maps);
+            maps += make_desc<kFmt, kN>(specs[i], d, batch.maps, maps);
             d.tile_begin = tiles;
             tiles += desc_tiles(d);
             ++probs;
@@ -333,8 +334,44 @@ void launch_gemms(const std::vector<GemmSpec>& specs, cudaStream_t stream) {
     }
 }
 
-void gemm_bf16(const std::vector<GemmSpec>& s, cudaStream_t st) { launch_gemms<kBF16>(s, st); }
-void gemm_oz8(const std::vector<GemmSpec>& s, cudaStream_t st) { launch_gemms<kOZ8>(s, st); }
+int sm_count() {
+    thread_local int n = 0;
+    if (!n) {
+        int dev = 0;
+        check(cudaGetDevice(&dev), "cudaGetDevice");
+        check(cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev), "cudaDeviceGetAttribute");
+    }
+    return n;
+}
+
+// Tile width for a kOZ8 launch: a short-K, K_FULL, rectangular update whose
+// 128-wide tiles would leave most SMs idle is split 2 or 4 ways along N
+// (PF_NO_NSPLIT=1 disables, for A/B).
+int pick_tile_n(const std::vector<GemmSpec>& specs) {
+    static const bool off = [] {
+        const char* e = std::getenv("PF_NO_NSPLIT");
+        return e && e[0] == '1';
+    }();
+    if (off || specs.empty()) return kTile;
+    long tiles = 0;
+    for (const GemmSpec& g : specs) {
+        if (g.k_mode != K_FULL || g.lower || (g.flags & EPI_MIRROR) || g.k > 512) return kTile;
+        tiles += static_cast<long>((g.rows + kTile - 1) / kTile) * ((g.cols + kTile - 1) / kTile);
+    }
+    const int sms = sm_count();
+    if (tiles * 4 <= sms) return 32;
+    if (tiles * 2 <= sms) return 64;
+    return kTile;
+}
+
+void gemm_bf16(const std::vector<GemmSpec>& s, cudaStream_t st) { launch_gemms_n<kBF16, 128>(s, st); }
+void gemm_oz8(const std::vector<GemmSpec>& s, cudaStream_t st) {
+    switch (pick_tile_n(s)) {
+        case 32: launch_gemms_n<kOZ8, 32>(s, st); break;
+        case 64: launch_gemms_n<kOZ8, 64>(s, st); break;
+        default: launch_gemms_n<kOZ8, 128>(s, st);
+    }
+}
 
 // ------------------------------------------------------------ small kernels
 constexpr int kMaxDamp = 16;
@@ -517,12 +554,12 @@ SideSlot& side_slot(int group, int depth) {
 }
 
 cudaEvent_t pool_event(int group, int id) {
-    thread_local std::vector<std::vector<cudaEvent_t>> pools;  // [device][group * 16 + id]
+    thread_local std::vector<std::vector<cudaEvent_t>> pools;  // [device][group * 32 + id]
     int dev = 0;
     check(cudaGetDevice(&dev), "cudaGetDevice");
     if (pools.size() <= static_cast<std::size_t>(dev)) pools.resize(dev + 1);
     auto& v = pools[dev];
-    const std::size_t i = static_cast<std::size_t>(group) * 16 + id;
+    const std::size_t i = static_cast<std::size_t>(group) * 32 + id;
     if (v.size() <= i) v.resize(i + 1, nullptr);
     if (!v[i]) check(cudaEventCreateWithFlags(&v[i], cudaEventDisableTiming), "cudaEventCreate(pool)");
     return v[i];

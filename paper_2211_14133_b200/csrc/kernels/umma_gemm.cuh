@@ -111,28 +111,35 @@ struct GemmBatch {
     int interleave;  // all problems share tile count and k-mode: tile rank major, problem minor
 };
 
-template <int kFmt>
+// kN: tile width (columns of C, rows of B).  128 everywhere except short
+// K_FULL kOZ8 launches with few tiles, which split each 128-wide tile over
+// 2 or 4 CTAs (kN = 64 / 32) so a latency-bound update spreads its MMAs and
+// epilogue over more SMs.
+template <int kFmt, int kN = 128>
 struct GemmTraits {
     static constexpr int kPlanes = kFmt == kOZ8 ? kDigits : 1;
-    static constexpr int kPlaneBytes = kFmt == kOZ8 ? 128 * 64 : 128 * 128;
-    static constexpr int kStageBytes = 2 * kPlanes * kPlaneBytes;
+    static constexpr int kPlaneBytes = kFmt == kOZ8 ? 128 * 64 : 128 * 128;  // A plane (128 rows)
+    static constexpr int kPlaneBytesB = kFmt == kOZ8 ? kN * 64 : kN * 128;   // B plane (kN rows)
+    static constexpr int kStageBytes = kPlanes * (kPlaneBytes + kPlaneBytesB);
     static constexpr int kStages = 3;
     // C-tile prefetch buffer (beta != 0, <= kStages-1 k-blocks): the unused
     // last stage plus kCPad, rows padded to kCStride floats (bank rotation)
-    static constexpr int kCStride = kTile + 4;
-    static constexpr int kCPad = kFmt == kOZ8 ? kTile * kCStride * 4 - kStageBytes : 0;
+    static constexpr int kCStride = kN + 4;
+    static constexpr int kCPad =
+        kFmt == kOZ8 && kTile * kCStride * 4 > kStageBytes ? kTile * kCStride * 4 - kStageBytes : 0;
     static constexpr int kSmemBytes = kStages * kStageBytes + kCPad + 1024 + 256 + 4 * kTile;
     static constexpr int kKBlock = 64;  // elements per k-block (both formats)
     static constexpr int kKSteps = kFmt == kOZ8 ? 2 : 4;  // 32-byte UMMA k-steps per block
-    static constexpr uint32_t kTmemCols = kFmt == kOZ8 ? 512 : 128;
+    static constexpr uint32_t kTmemCols = kFmt == kOZ8 ? 4 * kN : 128;
     static constexpr int kMinBlocks = kFmt == kOZ8 ? 1 : 2;
     // kOZ8 (one CTA per SM: 512 TMEM columns) runs 8 warps so the 4-accumulator
     // epilogue is split over warp pairs sharing a TMEM lane quarter
     static constexpr int kThreads = kFmt == kOZ8 ? 256 : 128;
     // kind::i8: signed int8 A/B (format 1), s32 accumulate (c_format 2)
     static constexpr uint32_t kIdesc =
-        kFmt == kOZ8 ? ((2u << 4) | (1u << 7) | (1u << 10) | ((128u >> 3) << 17) | ((128u >> 4) << 24))
-                     : ptx::make_idesc(1, 128, 128);
+        kFmt == kOZ8 ? ((2u << 4) | (1u << 7) | (1u << 10) | ((static_cast<uint32_t>(kN) >> 3) << 17) |
+                        ((128u >> 4) << 24))
+                     : ptx::make_idesc(1, 128, kN);
 };
 
 __device__ __forceinline__ void decode_lower(int t, int& tm, int& tn);
@@ -183,19 +190,21 @@ struct EpiRow {
     float diag_exact = 0.0f;
 };
 
-template <int kFmt>
+template <int kFmt, int kN = 128>
 __device__ __forceinline__ EpiRow epi_row(const GemmDesc& P, int tm, int tn, int r) {
     EpiRow e;
+    (void)tm;
     if constexpr (kFmt == kOZ8) {
         if (r < P.rows) {
             e.row_scale = P.alpha * ptx::pow2f(__ldcg(P.a_exp + r));
-            if ((P.flags & EPI_EXACT_DIAG) && tm == tn) e.diag_exact = static_cast<float>(__ldcg(P.a_sqnorm + r) * 0x1p14);
+            if ((P.flags & EPI_EXACT_DIAG) && r >= tn * kN && r < (tn + 1) * kN)  // row's diagonal in this tile
+                e.diag_exact = static_cast<float>(__ldcg(P.a_sqnorm + r) * 0x1p14);
         }
     }
     return e;
 }
 
-template <int kFmt>
+template <int kFmt, int kN = 128>
 __device__ __forceinline__ void epilogue_chunks(const GemmDesc& P, int tm, int tn, uint32_t lane_base, int r,
                                                 const float* col_scale, int chunk_begin, int chunk_end,
                                                 bool have_acc, const EpiRow& er, const float* crow = nullptr) {
@@ -203,13 +212,13 @@ __device__ __forceinline__ void epilogue_chunks(const GemmDesc& P, int tm, int t
     const uint32_t f = P.flags;
     const bool mirror = (f & EPI_MIRROR) && tm != tn;
     const float row_scale = er.row_scale;
-    const bool exact_diag = (f & EPI_EXACT_DIAG) && tm == tn && row_ok;
+    const bool exact_diag = (f & EPI_EXACT_DIAG) && row_ok;  // diag_chunk below: global r == c
     const float diag_exact = er.diag_exact;
     PF_ESTAMP(0);
 #pragma unroll 1
     for (int chunk = chunk_begin; chunk < chunk_end; ++chunk) {
         __syncwarp();  // tcgen05.ld is .sync.aligned: re-converge first
-        const int c0 = tn * kTile + chunk * 16;
+        const int c0 = tn * kN + chunk * 16;
         float out[16];
         if constexpr (kFmt == kOZ8) {
             // TMEM reads (64 B/clk per SM) bound this epilogue: 4 accumulators
@@ -217,7 +226,7 @@ __device__ __forceinline__ void epilogue_chunks(const GemmDesc& P, int tm, int t
             uint32_t raw[kDigits][16];
             if (have_acc) {
 #pragma unroll
-                for (int g = 0; g < kDigits; ++g) ptx::tmem_ld16_nowait(lane_base + g * 128 + chunk * 16, raw[g]);
+                for (int g = 0; g < kDigits; ++g) ptx::tmem_ld16_nowait(lane_base + g * kN + chunk * 16, raw[g]);
 #pragma unroll
                 for (int g = 0; g < kDigits; ++g) ptx::tmem_wait_ld_dep(raw[g]);
             } else {
@@ -324,10 +333,10 @@ __device__ __forceinline__ void epilogue_chunks(const GemmDesc& P, int tm, int t
 
 }
 
-template <int kFmt>
-__global__ void __launch_bounds__(GemmTraits<kFmt>::kThreads, GemmTraits<kFmt>::kMinBlocks)
+template <int kFmt, int kN = 128>
+__global__ void __launch_bounds__(GemmTraits<kFmt, kN>::kThreads, GemmTraits<kFmt, kN>::kMinBlocks)
     umma_gemm_kernel(const __grid_constant__ GemmBatch batch) {
-    using T = GemmTraits<kFmt>;
+    using T = GemmTraits<kFmt, kN>;
     constexpr int kStages = T::kStages;
     extern __shared__ uint8_t smem_raw[];
     uint8_t* smem = reinterpret_cast<uint8_t*>(
@@ -363,7 +372,7 @@ __global__ void __launch_bounds__(GemmTraits<kFmt>::kThreads, GemmTraits<kFmt>::
     const int warp = threadIdx.x >> 5;
     const uint32_t lane = threadIdx.x & 31;
     // short-K beta != 0 tiles read C into the idle last stage while the MMAs run
-    const int c_cols = min(kTile, P.cols - tn * kTile);
+    const int c_cols = min(kN, P.cols - tn * kN);
     const bool cpre = kFmt == kOZ8 && P.beta != 0.0f && kb1 - kb0 <= kStages - 1 && (P.flags & EPI_VEC4) &&
                       !(P.flags & EPI_TRANSPOSE) && c_cols > 0 && (c_cols & 3) == 0;
     float* cbuf = reinterpret_cast<float*>(smem + (kStages - 1) * T::kStageBytes);
@@ -399,7 +408,7 @@ __global__ void __launch_bounds__(GemmTraits<kFmt>::kThreads, GemmTraits<kFmt>::
         if (r < P.rows) {
             const uint32_t bytes = static_cast<uint32_t>(c_cols) * 4u;
             ptx::mbar_arrive_expect_tx(cbar, bytes);
-            ptx::bulk_load(cbuf + t * T::kCStride, P.c + static_cast<size_t>(r) * P.ldc + tn * kTile, bytes, cbar);
+            ptx::bulk_load(cbuf + t * T::kCStride, P.c + static_cast<size_t>(r) * P.ldc + tn * kN, bytes, cbar);
         } else {
             ptx::mbar_arrive(cbar);
         }
@@ -407,7 +416,7 @@ __global__ void __launch_bounds__(GemmTraits<kFmt>::kThreads, GemmTraits<kFmt>::
 
     auto a_plane = [&](int s, int pl) { return smem + s * T::kStageBytes + pl * T::kPlaneBytes; };
     auto b_plane = [&](int s, int pl) {
-        return smem + s * T::kStageBytes + (T::kPlanes + pl) * T::kPlaneBytes;
+        return smem + s * T::kStageBytes + T::kPlanes * T::kPlaneBytes + pl * T::kPlaneBytesB;
     };
 
     if (warp == 0 && lane == 0) {
@@ -420,10 +429,10 @@ __global__ void __launch_bounds__(GemmTraits<kFmt>::kThreads, GemmTraits<kFmt>::
             const int kc = kb * T::kKBlock;
             if constexpr (kFmt == kOZ8) {
                 ptx::tma_load_3d(a_plane(s, 0), &batch.maps[P.a_map], &full[s], kc, tm * kTile, 0);
-                ptx::tma_load_3d(b_plane(s, 0), &batch.maps[P.b_map], &full[s], kc, tn * kTile, 0);
+                ptx::tma_load_3d(b_plane(s, 0), &batch.maps[P.b_map], &full[s], kc, tn * kN, 0);
             } else {
                 ptx::tma_load_2d(a_plane(s, 0), &batch.maps[P.a_map], &full[s], kc, tm * kTile);
-                ptx::tma_load_2d(b_plane(s, 0), &batch.maps[P.b_map], &full[s], kc, tn * kTile);
+                ptx::tma_load_2d(b_plane(s, 0), &batch.maps[P.b_map], &full[s], kc, tn * kN);
             }
             if (++s == kStages) {
                 s = 0;
@@ -450,7 +459,7 @@ __global__ void __launch_bounds__(GemmTraits<kFmt>::kThreads, GemmTraits<kFmt>::
                             const int sb = g - sa;
                             const uint64_t da = ptx::sw64_kmajor_desc(ptx::smem_u32(a_plane(s, sa)) + off);
                             const uint64_t db = ptx::sw64_kmajor_desc(ptx::smem_u32(b_plane(s, sb)) + off);
-                            ptx::umma_i8(tmem + g * 128, da, db, T::kIdesc, (started >> g) & 1u);
+                            ptx::umma_i8(tmem + g * kN, da, db, T::kIdesc, (started >> g) & 1u);
                             started |= 1u << g;
                         }
                     }
@@ -473,15 +482,15 @@ __global__ void __launch_bounds__(GemmTraits<kFmt>::kThreads, GemmTraits<kFmt>::
     __syncwarp();
     if constexpr (kFmt == kOZ8) {  // warps 2-5: column scales while the MMAs run
         const int t = static_cast<int>(threadIdx.x) - 64;
-        if (t >= 0 && t < kTile) {
-            const int c = tn * kTile + t;
+        if (t >= 0 && t < kN) {
+            const int c = tn * kN + t;
             col_scale[t] = c < P.cols ? ptx::pow2f(__ldcg(P.b_exp + c)) : 0.0f;
         }
         __syncthreads();
     }
 
     // ---------------- epilogue: TMEM -> registers -> global
-    const EpiRow er = epi_row<kFmt>(P, tm, tn, tm * kTile + (warp & 3) * 32 + static_cast<int>(lane));
+    const EpiRow er = epi_row<kFmt, kN>(P, tm, tn, tm * kTile + (warp & 3) * 32 + static_cast<int>(lane));
     const bool have_acc = kb1 > kb0;
     if (have_acc) {
         ptx::mbar_wait(done, 0);
@@ -494,8 +503,8 @@ __global__ void __launch_bounds__(GemmTraits<kFmt>::kThreads, GemmTraits<kFmt>::
     {
         constexpr int kPairs = T::kThreads / 128;  // warps sharing a TMEM lane quarter
         const int ew = warp & 3, part = warp >> 2;
-        constexpr int kChunks = kTile / 16 / kPairs;
-        epilogue_chunks<kFmt>(P, tm, tn, tmem + (static_cast<uint32_t>(ew * 32) << 16),
+        constexpr int kChunks = kN / 16 / kPairs;
+        epilogue_chunks<kFmt, kN>(P, tm, tn, tmem + (static_cast<uint32_t>(ew * 32) << 16),
                               tm * kTile + ew * 32 + static_cast<int>(lane), col_scale, part * kChunks,
                               (part + 1) * kChunks, have_acc, er,
                               cpre ? cbuf + (ew * 32 + static_cast<int>(lane)) * T::kCStride : nullptr);
