@@ -579,9 +579,13 @@ struct StreamEmitter final : Emitter {
     cudaStream_t main;
     int group;
     int prio_main, prio_side, prio;  // launch priorities: critical chain high, side branches low
-    explicit StreamEmitter(cudaStream_t s, int g = 0) : st(s), main(s), group(g) {
+    // `lead`: the group has the largest factor size of the call (the longest
+    // chain).  Only lead chains get the top priority; the shorter groups run
+    // entirely at the lowest, filling the SMs the lead chain leaves idle
+    // (2x4096 + 10x1024: 3.07 -> 2.97 ms).
+    explicit StreamEmitter(cudaStream_t s, int g = 0, bool lead = true) : st(s), main(s), group(g) {
         const auto [least, greatest] = prio_range();
-        prio_main = prio = greatest;
+        prio_main = prio = lead ? greatest : least;
         prio_side = least;
     }
     void side_begin(int depth) override {
@@ -1612,7 +1616,7 @@ int pf_damped_inverse_batched(const pf_inverse_problem* problems, int count, voi
             run_program(groups, st);  // one persistent launch for every group
         } else {
             run_forked(groups.size(), st, [&](std::size_t g, cudaStream_t s) {
-                StreamEmitter em(s, static_cast<int>(g));
+                StreamEmitter em(s, static_cast<int>(g), groups[g].front()->d == groups[0].front()->d);
                 damped_inverse_group(groups[g], em, recursive);
             });
         }
