@@ -225,10 +225,12 @@ __device__ __forceinline__ void epilogue_chunks(const GemmDesc& P, int tm, int t
             // x 64 KB per tile
             uint32_t raw[kDigits][16];
             if (have_acc) {
+                if (chunk == chunk_begin + 1) PF_ESTAMP(6);
 #pragma unroll
                 for (int g = 0; g < kDigits; ++g) ptx::tmem_ld16_nowait(lane_base + g * kN + chunk * 16, raw[g]);
 #pragma unroll
                 for (int g = 0; g < kDigits; ++g) ptx::tmem_wait_ld_dep(raw[g]);
+                if (chunk == chunk_begin + 1) PF_ESTAMP(7);
             } else {
 #pragma unroll
                 for (int g = 0; g < kDigits; ++g)

@@ -34,8 +34,8 @@ prev = None
 for i in range(n):
     r = h[16 * i: 16 * i + 16]
     rel = [r[j] - r[0] for j in range(1, 6)]
-    epi = [r[j] - r[4] for j in range(6, 12)]
+    epi = [r[j] - r[4] for j in range(6, 14)]
     gap = (r[1] - prev) if prev else 0
     prev = r[5]
     print(f"{i:2d} {r[14]}x{r[15]} " + " ".join(f"{nm}+{v}" for nm, v in zip(names, rel)) + f"  (since prev end {gap} ns)"
-          + "  epi: scales+%d tmem0+%d chunks %s" % (epi[0], epi[1], [e for e in epi[2:]]))
+          + "  epi: scales+%d tmem0+%d chunks %s tmem1 %d..%d" % (epi[0], epi[1], [e for e in epi[2:6]], epi[6], epi[7]))
