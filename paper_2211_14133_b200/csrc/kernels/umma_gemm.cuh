@@ -198,12 +198,13 @@ __device__ __forceinline__ EpiRow epi_row(const GemmDesc& P, int tm, int tn, int
         if (r < P.rows) {
             e.row_scale = P.alpha * ptx::pow2f(__ldcg(P.a_exp + r));
             if ((P.flags & EPI_EXACT_DIAG) && r >= tn * kN && r < (tn + 1) * kN)  // row's diagonal in this tile
-                e.diag_exact = static_cast<float>(__ldcg(P.a_sqnorm + r) * 0x1p14);
+                e.diag_exact = static_cast<float>(__ldcg(P.a_sqnorm + r));  // = (norm 2^14) 2^-14
         }
     }
     return e;
 }
 
+// col_scale: kOZ8 -> 2^e_b per tile column, kBF16 -> unused.
 template <int kFmt, int kN = 128>
 __device__ __forceinline__ void epilogue_chunks(const GemmDesc& P, int tm, int tn, uint32_t lane_base, int r,
                                                 const float* col_scale, int chunk_begin, int chunk_end,
@@ -215,44 +216,130 @@ __device__ __forceinline__ void epilogue_chunks(const GemmDesc& P, int tm, int t
     const bool exact_diag = (f & EPI_EXACT_DIAG) && row_ok;  // diag_chunk below: global r == c
     const float diag_exact = er.diag_exact;
     PF_ESTAMP(0);
-#pragma unroll 1
-    for (int chunk = chunk_begin; chunk < chunk_end; ++chunk) {
-        __syncwarp();  // tcgen05.ld is .sync.aligned: re-converge first
+    // beta * C and the stores of one 16-column chunk
+    auto finish = [&](float (&out)[16], int chunk) {
         const int c0 = tn * kN + chunk * 16;
-        float out[16];
-        if constexpr (kFmt == kOZ8) {
-            // TMEM reads (64 B/clk per SM) bound this epilogue: 4 accumulators
-            // x 64 KB per tile
-            uint32_t raw[kDigits][16];
-            if (have_acc) {
-                if (chunk == chunk_begin + 1) PF_ESTAMP(6);
+        if (!row_ok || c0 >= P.cols) return;
+        const bool full_chunk = c0 + 16 <= P.cols;
+        if (P.beta != 0.0f) {
+            float cv[16];
+            if (crow && full_chunk) {  // C row prefetched into shared memory
+                const float4* src = reinterpret_cast<const float4*>(crow + chunk * 16);
 #pragma unroll
-                for (int g = 0; g < kDigits; ++g) ptx::tmem_ld16_nowait(lane_base + g * kN + chunk * 16, raw[g]);
+                for (int q = 0; q < 4; ++q) {
+                    const float4 t = src[q];
+                    cv[4 * q] = t.x;
+                    cv[4 * q + 1] = t.y;
+                    cv[4 * q + 2] = t.z;
+                    cv[4 * q + 3] = t.w;
+                }
+            } else if ((f & EPI_VEC4) && full_chunk && !(f & EPI_TRANSPOSE)) {
+                const float4* src = reinterpret_cast<const float4*>(P.c + static_cast<size_t>(r) * P.ldc + c0);
 #pragma unroll
-                for (int g = 0; g < kDigits; ++g) ptx::tmem_wait_ld_dep(raw[g]);
-                if (chunk == chunk_begin + 1) PF_ESTAMP(7);
+                for (int q = 0; q < 4; ++q) {
+                    const float4 t = __ldcg(src + q);
+                    cv[4 * q] = t.x;
+                    cv[4 * q + 1] = t.y;
+                    cv[4 * q + 2] = t.z;
+                    cv[4 * q + 3] = t.w;
+                }
             } else {
 #pragma unroll
-                for (int g = 0; g < kDigits; ++g)
-#pragma unroll
-                    for (int j = 0; j < 16; ++j) raw[g][j] = 0u;
+                for (int j = 0; j < 16; ++j) {
+                    const int c = c0 + j;
+                    const size_t idx = (f & EPI_TRANSPOSE) ? static_cast<size_t>(c) * P.ldc + r
+                                                           : static_cast<size_t>(r) * P.ldc + c;
+                    cv[j] = c < P.cols ? __ldcg(P.c + idx) : 0.0f;
+                }
             }
+#pragma unroll
+            for (int j = 0; j < 16; ++j) out[j] = fmaf(P.beta, cv[j], out[j]);
+        }
+#ifdef PF_PROBE_NOSTORE
+        if (P.beta != 0.0f && P.rows <= kTile && P.cols <= kTile) {
+            if (out[0] == 12345.678f) P.c[0] = out[1];  // keep the values live
+            return;
+        }
+#endif
+        if ((f & EPI_VEC4) && full_chunk && !(f & EPI_TRANSPOSE)) {
+            float4* dst = reinterpret_cast<float4*>(P.c + static_cast<size_t>(r) * P.ldc + c0);
+#pragma unroll
+            for (int q = 0; q < 4; ++q)
+                dst[q] = make_float4(out[4 * q], out[4 * q + 1], out[4 * q + 2], out[4 * q + 3]);
+        } else if (f & EPI_TRANSPOSE) {
+            // lanes hold consecutive rows -> each transposed column store is coalesced
+#pragma unroll
+            for (int j = 0; j < 16; ++j)
+                if (c0 + j < P.cols) P.c[static_cast<size_t>(c0 + j) * P.ldc + r] = out[j];
+        } else {
+#pragma unroll
+            for (int j = 0; j < 16; ++j)
+                if (c0 + j < P.cols) P.c[static_cast<size_t>(r) * P.ldc + c0 + j] = out[j];
+        }
+        if (mirror) {
+#pragma unroll
+            for (int j = 0; j < 16; ++j)
+                if (c0 + j < P.cols) P.c[static_cast<size_t>(c0 + j) * P.ldc + r] = out[j];
+        }
+        if (f & EPI_ALSO_T) {
+#pragma unroll
+            for (int j = 0; j < 16; ++j)
+                if (c0 + j < P.cols) P.c_t[static_cast<size_t>(c0 + j) * P.ldc_t + r] = out[j];
+        }
+    };
+    // the diagonal of a same-operand product: exact norm of the represented row
+    auto diag_fix = [&](float (&out)[16], int chunk) {
+        const int c0 = tn * kN + chunk * 16;
+        if (exact_diag && r >= c0 && r < c0 + 16) {
+#pragma unroll
+            for (int j = 0; j < 16; ++j)
+                if (c0 + j == r) out[j] = (row_scale * col_scale[chunk * 16 + j]) * diag_exact;
+        }
+    };
+    if constexpr (kFmt == kOZ8) {
+        if (!have_acc) {  // empty k-range
+#pragma unroll 1
+            for (int chunk = chunk_begin; chunk < chunk_end; ++chunk) {
+                float out[16];
+#pragma unroll
+                for (int j = 0; j < 16; ++j) out[j] = 0.0f;
+                diag_fix(out, chunk);
+                finish(out, chunk);
+            }
+            return;
+        }
+#pragma unroll 1
+        for (int chunk = chunk_begin; chunk < chunk_end; ++chunk) {
+            __syncwarp();  // tcgen05.ld is .sync.aligned: re-converge first
+            uint32_t raw[kDigits][16];
+            if (chunk == chunk_begin + 1) PF_ESTAMP(6);
+#pragma unroll
+            for (int g = 0; g < kDigits; ++g) ptx::tmem_ld16_nowait(lane_base + g * kN + chunk * 16, raw[g]);
+#pragma unroll
+            for (int g = 0; g < kDigits; ++g) ptx::tmem_wait_ld_dep(raw[g]);
+            if (chunk == chunk_begin + 1) PF_ESTAMP(7);
             if (chunk == chunk_begin) PF_ESTAMP(1);
             // accumulator g counts units of 2^-7(g+2) of 2^(e_a + e_b); the four
             // exact int32 sums are recombined smallest-first in fp32 (the result
             // is stored in fp32: ~1 ulp, no accumulation error)
-            const bool diag_chunk = exact_diag && r >= c0 && r < c0 + 16;
+            float out[16];
 #pragma unroll
             for (int j = 0; j < 16; ++j) {
-                float s = static_cast<float>(static_cast<int>(raw[3][j])) * 0x1p-21f;
-                s = fmaf(static_cast<float>(static_cast<int>(raw[2][j])), 0x1p-14f, s);
-                s = fmaf(static_cast<float>(static_cast<int>(raw[1][j])), 0x1p-7f, s);
-                s = fmaf(static_cast<float>(static_cast<int>(raw[0][j])), 1.0f, s);
-                if (diag_chunk && c0 + j == r)
-                    s = diag_exact;  // exact sum of squares of the represented row
-                out[j] = (row_scale * col_scale[chunk * 16 + j]) * (s * 0x1p-14f);
+                // (the product's 2^-14 is folded into the digit weights: exact)
+                float s = static_cast<float>(static_cast<int>(raw[3][j])) * 0x1p-35f;
+                s = fmaf(static_cast<float>(static_cast<int>(raw[2][j])), 0x1p-28f, s);
+                s = fmaf(static_cast<float>(static_cast<int>(raw[1][j])), 0x1p-21f, s);
+                s = fmaf(static_cast<float>(static_cast<int>(raw[0][j])), 0x1p-14f, s);
+                out[j] = (row_scale * col_scale[chunk * 16 + j]) * s;
             }
-        } else {
+            diag_fix(out, chunk);
+            finish(out, chunk);
+            if (chunk - chunk_begin < 4) PF_ESTAMP(2 + chunk - chunk_begin);
+        }
+    } else {
+#pragma unroll 1
+        for (int chunk = chunk_begin; chunk < chunk_end; ++chunk) {
+            __syncwarp();
             float v[16];
             if (have_acc) {
                 ptx::tmem_ld16(lane_base + chunk * 16, v);
@@ -260,79 +347,12 @@ __device__ __forceinline__ void epilogue_chunks(const GemmDesc& P, int tm, int t
 #pragma unroll
                 for (int j = 0; j < 16; ++j) v[j] = 0.0f;
             }
+            float out[16];
 #pragma unroll
             for (int j = 0; j < 16; ++j) out[j] = P.alpha * v[j];
+            finish(out, chunk);
         }
-        if (row_ok && c0 < P.cols) {
-            const bool full_chunk = c0 + 16 <= P.cols;
-            if (P.beta != 0.0f) {
-                float cv[16];
-                if (crow && full_chunk) {  // C row prefetched into shared memory
-                    const float4* src = reinterpret_cast<const float4*>(crow + chunk * 16);
-#pragma unroll
-                    for (int q = 0; q < 4; ++q) {
-                        const float4 t = src[q];
-                        cv[4 * q] = t.x;
-                        cv[4 * q + 1] = t.y;
-                        cv[4 * q + 2] = t.z;
-                        cv[4 * q + 3] = t.w;
-                    }
-                } else if ((f & EPI_VEC4) && full_chunk && !(f & EPI_TRANSPOSE)) {
-                    const float4* src = reinterpret_cast<const float4*>(P.c + static_cast<size_t>(r) * P.ldc + c0);  // read via ld.cg below
-#pragma unroll
-                    for (int q = 0; q < 4; ++q) {
-                        const float4 t = __ldcg(src + q);
-                        cv[4 * q] = t.x;
-                        cv[4 * q + 1] = t.y;
-                        cv[4 * q + 2] = t.z;
-                        cv[4 * q + 3] = t.w;
-                    }
-                } else {
-#pragma unroll
-                    for (int j = 0; j < 16; ++j) {
-                        const int c = c0 + j;
-                        const size_t idx = (f & EPI_TRANSPOSE) ? static_cast<size_t>(c) * P.ldc + r
-                                                               : static_cast<size_t>(r) * P.ldc + c;
-                        cv[j] = c < P.cols ? __ldcg(P.c + idx) : 0.0f;
-                    }
-                }
-#pragma unroll
-                for (int j = 0; j < 16; ++j) out[j] = fmaf(P.beta, cv[j], out[j]);
-            }
-#ifdef PF_PROBE_NOSTORE
-            if (P.beta != 0.0f && P.rows <= kTile && P.cols <= kTile) {
-                if (out[0] == 12345.678f) P.c[0] = out[1];  // keep the values live
-            } else
-#endif
-            if ((f & EPI_VEC4) && full_chunk && !(f & EPI_TRANSPOSE)) {
-                float4* dst = reinterpret_cast<float4*>(P.c + static_cast<size_t>(r) * P.ldc + c0);
-#pragma unroll
-                for (int q = 0; q < 4; ++q)
-                    dst[q] = make_float4(out[4 * q], out[4 * q + 1], out[4 * q + 2], out[4 * q + 3]);
-            } else if (f & EPI_TRANSPOSE) {
-                // lanes hold consecutive rows -> each transposed column store is coalesced
-#pragma unroll
-                for (int j = 0; j < 16; ++j)
-                    if (c0 + j < P.cols) P.c[static_cast<size_t>(c0 + j) * P.ldc + r] = out[j];
-            } else {
-#pragma unroll
-                for (int j = 0; j < 16; ++j)
-                    if (c0 + j < P.cols) P.c[static_cast<size_t>(r) * P.ldc + c0 + j] = out[j];
-            }
-            if (mirror) {
-#pragma unroll
-                for (int j = 0; j < 16; ++j)
-                    if (c0 + j < P.cols) P.c[static_cast<size_t>(c0 + j) * P.ldc + r] = out[j];
-            }
-            if (f & EPI_ALSO_T) {
-#pragma unroll
-                for (int j = 0; j < 16; ++j)
-                    if (c0 + j < P.cols) P.c_t[static_cast<size_t>(c0 + j) * P.ldc_t + r] = out[j];
-            }
-        }
-        if (chunk - chunk_begin < 4) PF_ESTAMP(2 + chunk - chunk_begin);
     }
-
 }
 
 template <int kFmt, int kN = 128>
