@@ -315,13 +315,39 @@ def run_gpu_arm(args, rank, world, local_rank):
     # compute (double-buffered device inputs, copy engines on their own
     # streams): H2D(k+1) || compute(k) || D2H(k-1).  All of it is inside the
     # timed region.
-    h_tapes = [x.cpu().pin_memory() for x in st.tapes]
-    h_grads = [g.cpu().pin_memory() for g in st.grads]
-    h_w = [w.cpu().pin_memory() for w in st.weights]
-    h2d = sum(t.numel() * t.element_size() for t in h_tapes + h_grads)
-    d2h = sum(t.numel() * t.element_size() for t in h_w)
-    sets = [(st.tapes, st.grads), ([torch.empty_like(x) for x in st.tapes], [torch.empty_like(g) for g in st.grads])]
-    w_snaps = [[torch.empty_like(w) for w in st.weights] for _ in (0, 1)]
+    # Inputs and outputs are packed into ONE pinned host buffer each way and
+    # the device tensors are views of one buffer per double-buffer slot, so
+    # every step is one H2D and one D2H copy (18 separate copies per step
+    # cost ~0.4 ms of per-copy overhead on a copy engine that is already the
+    # e2e bound: 201 MB at ~55 GB/s).
+    def packed(tensors):
+        offs, total = [], 0
+        for t in tensors:
+            offs.append(total)
+            total += (t.numel() * t.element_size() + 255) // 256 * 256
+        return offs, total
+
+    def views(buf, tensors, offs):
+        return [buf[o:o + t.numel() * t.element_size()].view(t.dtype).view(t.shape) for t, o in zip(tensors, offs)]
+
+    ins = list(st.tapes) + list(st.grads)
+    in_offs, in_total = packed(ins)
+    h_in = torch.empty(in_total, dtype=torch.uint8).pin_memory()
+    for hv, t in zip(views(h_in, ins, in_offs), ins):
+        hv.copy_(t.cpu())
+    out_offs, out_total = packed(st.weights)
+    h_out = torch.empty(out_total, dtype=torch.uint8).pin_memory()
+    h2d = sum(t.numel() * t.element_size() for t in ins)
+    d2h = sum(t.numel() * t.element_size() for t in st.weights)
+    d_in = [torch.empty(in_total, dtype=torch.uint8, device="cuda") for _ in (0, 1)]
+    sets = []
+    for buf in d_in:
+        vs = views(buf, ins, in_offs)
+        for v, t in zip(vs, ins):
+            v.copy_(t)
+        sets.append((vs[:len(st.tapes)], vs[len(st.tapes):]))
+    d_out = [torch.empty(out_total, dtype=torch.uint8, device="cuda") for _ in (0, 1)]
+    w_snaps = [views(buf, st.weights, out_offs) for buf in d_out]
     copy_in = torch.cuda.Stream()
     copy_out = torch.cuda.Stream()
 
@@ -346,12 +372,8 @@ def run_gpu_arm(args, rank, world, local_rank):
     torch.cuda.synchronize()
 
     def h2d_into(k):
-        tapes, grads = sets[k % 2]
         with torch.cuda.stream(copy_in):
-            for h, d in zip(h_tapes, tapes):
-                d.copy_(h, non_blocking=True)
-            for h, d in zip(h_grads, grads):
-                d.copy_(h, non_blocking=True)
+            d_in[k % 2].copy_(h_in, non_blocking=True)
         ev = torch.cuda.Event()
         ev.record(copy_in)
         return ev
@@ -374,8 +396,7 @@ def run_gpu_arm(args, rank, world, local_rank):
                 in_ready.append(h2d_into(k + 1))
             copy_out.wait_event(ev)
             with torch.cuda.stream(copy_out):
-                for h, d in zip(h_w, w_snaps[k % 2]):
-                    h.copy_(d, non_blocking=True)
+                h_out.copy_(d_out[k % 2], non_blocking=True)
             od = torch.cuda.Event()
             od.record(copy_out)
             out_done.append(od)

@@ -1,0 +1,27 @@
+import torch, time
+torch.cuda.set_device(0)
+n = 201 * 1024 * 1024
+h = torch.empty(n, dtype=torch.uint8).pin_memory()
+d = torch.empty(n, dtype=torch.uint8, device="cuda")
+hb = torch.empty(50 * 1024 * 1024, dtype=torch.uint8).pin_memory()
+db = torch.empty(50 * 1024 * 1024, dtype=torch.uint8, device="cuda")
+s1, s2, s3 = torch.cuda.Stream(), torch.cuda.Stream(), torch.cuda.Stream()
+def t(fn, reps=5):
+    fn(); torch.cuda.synchronize()
+    e0 = torch.cuda.Event(enable_timing=True); e1 = torch.cuda.Event(enable_timing=True)
+    e0.record()
+    for _ in range(reps): fn()
+    e1.record(); torch.cuda.synchronize()
+    return e0.elapsed_time(e1) / reps
+def one(): d.copy_(h, non_blocking=True)
+def two():
+    half = n // 2
+    with torch.cuda.stream(s1): d[:half].copy_(h[:half], non_blocking=True)
+    with torch.cuda.stream(s2): d[half:].copy_(h[half:], non_blocking=True)
+    torch.cuda.current_stream().wait_stream(s1); torch.cuda.current_stream().wait_stream(s2)
+def with_d2h():
+    with torch.cuda.stream(s1): d.copy_(h, non_blocking=True)
+    with torch.cuda.stream(s3): hb.copy_(db, non_blocking=True)
+    torch.cuda.current_stream().wait_stream(s1); torch.cuda.current_stream().wait_stream(s3)
+for name, fn in [("one", one), ("two streams", two), ("h2d+d2h", with_d2h)]:
+    ms = t(fn); print(f"{name:12s} {ms:.3f} ms  {n / ms / 1e6:.1f} GB/s")
