@@ -412,6 +412,12 @@ def run_gpu_arm(args, rank, world, local_rank):
     e1.record(stream)
     torch.cuda.synchronize()
     e2e_ms = e0.elapsed_time(e1) / args.steps
+    if os.environ.get("PF_BENCH_E2E_TRACE") and rank == 0:  # development: copy/compute timeline
+        from torch.profiler import ProfilerActivity, profile
+        with profile(activities=[ProfilerActivity.CUDA]) as prof:
+            e2e_run(4)
+            torch.cuda.synchronize()
+        prof.export_chrome_trace(os.environ["PF_BENCH_E2E_TRACE"])
     use(0)
     if dist:
         t = torch.tensor([e2e_ms], device="cuda")
