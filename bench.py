@@ -231,6 +231,10 @@ def run_gpu_arm(args, rank, world, local_rank):
             dist.all_reduce(f, op=dist.ReduceOp.AVG)
 
     def step(ev=None):
+        step_a(ev)
+        step_b(ev)
+
+    def step_a(ev=None):  # needs the tapes
         if ev: ev[0].record(stream)
         st.curvature()
         if ev: ev[1].record(stream)
@@ -244,6 +248,8 @@ def run_gpu_arm(args, rank, world, local_rank):
         else:
             st.invert()
         if ev: ev[2].record(stream)
+
+    def step_b(ev=None):  # needs the gradients
         st.precondition()
         if ev: ev[3].record(stream)
 
@@ -358,35 +364,47 @@ def run_gpu_arm(args, rank, world, local_rank):
         for w, sw in zip(st.weights, w_snaps[k % 2]):
             sw.copy_(w)
 
+    # each step in two parts: curvature + inversion need only the tapes, the
+    # preconditioner the gradients, so the first step starts once its tapes
+    # (3/4 of the bytes) are in and the gradients' copy overlaps the inversion
     runners = []
     for k in (0, 1):
         use(k)
         if world == 1 and not args.no_graph:
-            g2 = torch.cuda.CUDAGraph()
-            with torch.cuda.graph(g2):
-                step()
+            ga, gb = torch.cuda.CUDAGraph(), torch.cuda.CUDAGraph()
+            with torch.cuda.graph(ga):
+                step_a()
+            with torch.cuda.graph(gb):
+                step_b()
                 snapshot(k)
-            runners.append(g2.replay)
+            runners.append((ga.replay, gb.replay))
         else:
-            runners.append(lambda k=k: (step(), snapshot(k)))
+            runners.append((step_a, lambda k=k: (step_b(), snapshot(k))))
     torch.cuda.synchronize()
+    n_tape_bytes = in_offs[len(st.tapes)] if len(st.grads) else in_total
 
     def h2d_into(k):
+        evs = []
         with torch.cuda.stream(copy_in):
-            d_in[k % 2].copy_(h_in, non_blocking=True)
-        ev = torch.cuda.Event()
-        ev.record(copy_in)
-        return ev
+            d_in[k % 2][:n_tape_bytes].copy_(h_in[:n_tape_bytes], non_blocking=True)
+            evs.append(torch.cuda.Event())
+            evs[-1].record(copy_in)
+            d_in[k % 2][n_tape_bytes:].copy_(h_in[n_tape_bytes:], non_blocking=True)
+            evs.append(torch.cuda.Event())
+            evs[-1].record(copy_in)
+        return evs
 
     def e2e_run(n):
         in_ready = [h2d_into(0)]
         done, out_done = [], []
         for k in range(n):
-            stream.wait_event(in_ready[k])
+            stream.wait_event(in_ready[k][0])
             if k >= 2:                     # weight snapshot buffer k%2 read back by step k-2's D2H
                 stream.wait_event(out_done[k - 2])
             use(k)
-            runners[k % 2]()
+            runners[k % 2][0]()
+            stream.wait_event(in_ready[k][1])
+            runners[k % 2][1]()
             ev = torch.cuda.Event()
             ev.record(stream)
             done.append(ev)
@@ -490,7 +508,7 @@ def run_gpu_arm(args, rank, world, local_rank):
         "roofline_syrk": roof_syrk,
         "e2e": {"value": e2e_value, "unit": UNIT, "ms_per_step": e2e_ms,
                 "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
-                "overlap": "pinned host buffers; H2D(step k+1) || compute(k) || D2H(k-1), double-buffered inputs"},
+                "overlap": "pinned host buffers, one H2D for the tapes and one for the gradients per step (curvature + inversion start on the tapes, the preconditioner waits for the gradients), one D2H of the updated weights; H2D(step k+1) || compute(k) || D2H(k-1), double-buffered inputs; the copy engine (201 MB at ~55 GB/s) bounds the steady state"},
         "gpu_launches": launches // max(1, args.steps) if False else launches,
         "clocks": clocks.summary(),
         "cpu_baseline": cpu,
