@@ -527,7 +527,25 @@ struct Emitter {
     virtual void on(int) {}
     virtual void record(int) {}
     virtual void wait(int) {}
+    // lead chain progress mark (shorter groups of the same call start there)
+    virtual void mark_lead(int /*panel*/, int /*panels*/) {}
 };
+
+// A group with a SHORTER chain than the lead (smaller d) of a right-looking
+// call starts when the lead's factorisation reaches panel nb_lead - 2 nb_g:
+// started together it takes SMs from the lead's launch-latency-bound chain for
+// its whole length; started late it still finishes before the lead's TRTRI /
+// LAUUM tail (2x4096 + 10x1024, start panel of the 1024 groups: 0 -> 2.79 ms,
+// 4: 2.77, 10: 2.74, 16: 2.72, 22: 2.72, 28: 2.93).  PF_INV_DELAY=0 disables.
+bool lead_delay_enabled() {
+    static const bool on = [] {
+        const char* e = std::getenv("PF_INV_DELAY");
+        return !(e && e[0] == '0');
+    }();
+    return on;
+}
+constexpr int kMarkGroup = 1000;  // pool_event(kMarkGroup, panel): lead progress marks
+thread_local int g_lead_panels = 0;  // panels marked by the lead group of the current call
 
 // Per-thread, per-device pool of (stream, done event) pairs for the side
 // branches of the recursion, indexed by (group slot, depth).
@@ -603,6 +621,11 @@ struct StreamEmitter final : Emitter {
     }
     void side_join(int depth) override {
         check(cudaStreamWaitEvent(main, side_slot(group, depth).done, 0), "side join");
+    }
+    void mark_lead(int panel, int panels) override {
+        if (group != 0 || !lead_delay_enabled()) return;
+        check(cudaEventRecord(pool_event(kMarkGroup, panel), main), "cudaEventRecord(lead mark)");
+        g_lead_panels = std::max(g_lead_panels, std::min(panel + 1, panels));
     }
     void on(int s) override {
         st = s == 0 ? main : side_slot(group, 11 + s).stream;
@@ -903,6 +926,7 @@ void cholesky_blocked(const std::vector<InvWs>& ws, Emitter& em) {
     bool side_used[2] = {false, false};
     for (int k = 0; k < nb; ++k) {
         const int o = k * kLeaf;
+        em.mark_lead(k, nb);
         em.leaves(ws, o, std::min(kLeaf, d - o));
         if (k == nb - 1) break;
         const int r0 = o + kLeaf, m = d - r0, slot = k % 3;
@@ -1615,7 +1639,15 @@ int pf_damped_inverse_batched(const pf_inverse_problem* problems, int count, voi
         if (g_inverse_mode.load() == 1) {
             run_program(groups, st);  // one persistent launch for every group
         } else {
+            g_lead_panels = 0;
+            const int lead_d = groups[0].front()->d;
             run_forked(groups.size(), st, [&](std::size_t g, cudaStream_t s) {
+                const int d_g = groups[g].front()->d;
+                if (g > 0 && d_g < lead_d && g_lead_panels > 0) {
+                    const int start = g_lead_panels - 2 * ((d_g + kLeaf - 1) / kLeaf);
+                    if (start > 0)
+                        check(cudaStreamWaitEvent(s, pool_event(kMarkGroup, start), 0), "lead mark wait");
+                }
                 StreamEmitter em(s, static_cast<int>(g), groups[g].front()->d == groups[0].front()->d);
                 damped_inverse_group(groups[g], em, recursive);
             });
