@@ -10,6 +10,7 @@
 #include <cudaTypedefs.h>
 
 #include <algorithm>
+#include <functional>
 #include <cstdio>
 #include <cstdlib>
 #include <utility>
@@ -893,7 +894,8 @@ void inverse_rec(const std::vector<InvWs>& ws, int o, int n, Emitter& em, int de
 //   BR   the rest, columns >= k+3, lower (awaited by BU(k+1))             -> B
 // so the trailing update overlaps leaf(k+1) instead of preceding it.
 // w.l receives the strictly-lower L, w.x / w.xt the diagonal blocks of L^-1.
-void cholesky_blocked(const std::vector<InvWs>& ws, Emitter& em) {
+void cholesky_blocked(const std::vector<InvWs>& ws, Emitter& em,
+                      const std::function<void(int)>& after_leaf = nullptr) {
     const int d = ws.front().d;
     const int nb = (d + kLeaf - 1) / kLeaf;
     // event ids (per group, 16 available): F fork, A/U/B rings of 2, END per side stream
@@ -928,6 +930,7 @@ void cholesky_blocked(const std::vector<InvWs>& ws, Emitter& em) {
         const int o = k * kLeaf;
         em.mark_lead(k, nb);
         em.leaves(ws, o, std::min(kLeaf, d - o));
+        if (after_leaf) after_leaf(k);
         if (k == nb - 1) break;
         const int r0 = o + kLeaf, m = d - r0, slot = k % 3;
         const int nc = std::min(kLeaf, m);  // width of block column k+1
@@ -1089,10 +1092,18 @@ int tri_height(int n, std::vector<std::vector<TriNode>>& by_h, int o) {
     return h;
 }
 
-void trtri_levels(const std::vector<InvWs>& ws, Emitter& em) {
-    const int d = ws.front().d;
+void trtri_emit_levels(const std::vector<InvWs>& ws, Emitter& em, const std::vector<std::vector<TriNode>>& by_h);
+
+// Bottom-up TRTRI of the diagonal range [o, o + n) (its node tree as built by
+// tri_height: the whole matrix for (0, d), a subtree otherwise), every level
+// one slice + GEMM pair per phase for all nodes and problems.
+void trtri_levels(const std::vector<InvWs>& ws, Emitter& em, int o, int n) {
     std::vector<std::vector<TriNode>> by_h;
-    tri_height(d, by_h, 0);
+    tri_height(n, by_h, o);
+    trtri_emit_levels(ws, em, by_h);
+}
+
+void trtri_emit_levels(const std::vector<InvWs>& ws, Emitter& em, const std::vector<std::vector<TriNode>>& by_h) {
     for (const auto& level : by_h) {
         std::vector<SliceReq> sl;
         std::vector<GemmSpec> g;
@@ -1159,7 +1170,15 @@ void trtri_levels(const std::vector<InvWs>& ws, Emitter& em) {
 // latency-bound (right-looking wins: one BERT-Large layer, 3.5 -> 3.1 ms for
 // the two d = 4096 factors); a call with many is throughput-bound (recursive
 // wins: a 24-layer refresh, 60 -> 37 ms).  PF_INV_RECURSIVE=0/1 forces one.
-int g_recursive_from = 24;  // problems per call at which the recursive schedule takes over
+int g_recursive_from = 24;
+
+bool early_trtri_enabled() {  // PF_EARLY_TRTRI=0: whole TRTRI after the factorisation (A/B)
+    static const bool on = [] {
+        const char* e = std::getenv("PF_EARLY_TRTRI");
+        return !(e && e[0] == '0');
+    }();
+    return on;
+}  // problems per call at which the recursive schedule takes over
 
 bool use_recursive_inverse(int problems) {
     static const int forced = [] {
@@ -1183,8 +1202,35 @@ void damped_inverse_group(const std::vector<const pf_inverse_problem*>& probs, E
     if (recursive) {
         inverse_rec(ws, 0, d, em);
     } else {
-        cholesky_blocked(ws, em);
-        trtri_levels(ws, em);
+        // The TRTRI subtree of the root's left half [0, n1) needs only L and
+        // the leaves of panels < n1/128: it runs on a low-priority side stream
+        // under the rest of the factorisation (whose chain leaves most SMs
+        // idle); the right subtree and the root node follow the factorisation.
+        // (Streaming every finished node at its panel instead measured slower
+        // for the latency-bound calls: the many small nodes interfere with the
+        // chain; 2x4096 2.58 vs 2.53 ms.)
+        const int d = ws.front().d;
+        const int n1 = kTile * ((d + 2 * kTile - 1) / (2 * kTile));
+        std::vector<std::vector<TriNode>> left;
+        if (d > kLeaf) tri_height(n1, left, 0);
+        constexpr int evF = 29, evT = 30, kTrtriStream = 3;
+        const bool split = !left.empty() && early_trtri_enabled();
+        cholesky_blocked(ws, em, [&](int k) {
+            if (!split || k != n1 / kLeaf - 1) return;
+            em.record(evF);
+            em.on(kTrtriStream);
+            em.wait(evF);
+            trtri_emit_levels(ws, em, left);
+            em.record(evT);
+            em.on(0);
+        });
+        if (split) {
+            em.wait(evT);  // s0 / s1 level slots are reused by the right subtree
+            trtri_levels(ws, em, n1, d - n1);
+            trtri_emit_levels(ws, em, {{TriNode{0, n1, d - n1}}});
+        } else {
+            trtri_levels(ws, em, 0, d);
+        }
     }
     // ---- LAUUM: M^-1 = X^T X = XT XT^T  (lower tiles, mirrored)
     std::vector<SliceReq> sl;
