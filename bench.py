@@ -294,16 +294,44 @@ def run_gpu_arm(args, rank, world, local_rank):
     if dist: dist.barrier()
     ms = t_start.elapsed_time(t_end) / args.steps
 
-    # phase breakdown: a separate eager pass with events between the phases
-    evs = [[torch.cuda.Event(enable_timing=True) for _ in range(4)] for _ in range(args.steps)]
-    for i in range(args.steps):
-        step(evs[i])
-    torch.cuda.synchronize()
+    # phase breakdown.  Graphed: replays of the step's prefixes (curvature;
+    # curvature + inversion; the whole step), each timed alone with events, so
+    # the phases are measured as the step runs (the inversion's ~300 launches
+    # are host-bound when issued eagerly).  Otherwise an eager pass with events
+    # between the phases.
     phases = {"curvature": 0.0, "inversion": 0.0, "precondition": 0.0}
-    for e in evs:
-        phases["curvature"] += e[0].elapsed_time(e[1]) / args.steps
-        phases["inversion"] += e[1].elapsed_time(e[2]) / args.steps
-        phases["precondition"] += e[2].elapsed_time(e[3]) / args.steps
+    if graphed:
+        def prefix_graph(fn):
+            g = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(g):
+                fn()
+            return g
+
+        g_c = prefix_graph(st.curvature)
+        g_ci = prefix_graph(lambda: (st.curvature(), st.invert()))
+
+        def replay_ms(g):
+            g.replay()
+            torch.cuda.synchronize()
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record(stream)
+            for _ in range(args.steps):
+                g.replay()
+            e1.record(stream)
+            torch.cuda.synchronize()
+            return e0.elapsed_time(e1) / args.steps
+
+        t_c, t_ci, t_all = replay_ms(g_c), replay_ms(g_ci), replay_ms(graph)
+        phases = {"curvature": t_c, "inversion": t_ci - t_c, "precondition": t_all - t_ci}
+    else:
+        evs = [[torch.cuda.Event(enable_timing=True) for _ in range(4)] for _ in range(args.steps)]
+        for i in range(args.steps):
+            step(evs[i])
+        torch.cuda.synchronize()
+        for e in evs:
+            phases["curvature"] += e[0].elapsed_time(e[1]) / args.steps
+            phases["inversion"] += e[1].elapsed_time(e[2]) / args.steps
+            phases["precondition"] += e[2].elapsed_time(e[3]) / args.steps
     if dist:
         t = torch.tensor([ms], device="cuda")
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
