@@ -297,9 +297,15 @@ int make_desc(const GemmSpec& s, GemmDesc& d, CUtensorMap* maps, int n_maps) {
 inline int desc_tiles(const GemmDesc& d) { return d.lower ? d.tiles_m * (d.tiles_m + 1) / 2 : d.tiles_m * d.tiles_n; }
 
 template <int kFmt, int kN>
-void launch_gemms_n(const std::vector<GemmSpec>& specs, cudaStream_t stream) {
+void launch_gemms_n(const std::vector<GemmSpec>& specs_in, cudaStream_t stream) {
     using T = GemmTraits<kFmt, kN>;
     auto kernel = umma_gemm_kernel<kFmt, kN>;
+    // Longest per-tile K first (problems of one launch are independent): the
+    // block scheduler hands out CTAs roughly in blockIdx order, so long tiles
+    // queued last would run as a tail on few SMs (the preconditioner mixes
+    // K = 1024 and K = 4096 products in one launch).
+    std::vector<GemmSpec> specs(specs_in);
+    std::stable_sort(specs.begin(), specs.end(), [](const GemmSpec& a, const GemmSpec& b) { return a.k > b.k; });
     static std::once_flag attr_once;
     std::call_once(attr_once, [&] {
         check(cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, T::kSmemBytes),
