@@ -1172,11 +1172,15 @@ void trtri_emit_levels(const std::vector<InvWs>& ws, Emitter& em, const std::vec
 // Two schedules of the same factorisation: the right-looking one (above) has
 // the shortest critical path but re-reads / re-writes the trailing matrix once
 // per 128-column panel (K = 128 updates); the recursive one (inverse_rec)
-// aggregates those updates into large-K GEMMs.  A call with few factors is
-// latency-bound (right-looking wins: one BERT-Large layer, 3.5 -> 3.1 ms for
-// the two d = 4096 factors); a call with many is throughput-bound (recursive
-// wins: a 24-layer refresh, 60 -> 37 ms).  PF_INV_RECURSIVE=0/1 forces one.
-int g_recursive_from = 24;
+// aggregates those updates into large-K GEMMs.  A call is latency-bound while
+// its total work per panel of the longest chain, W = sum d^3 / d_max, is small
+// (right-looking wins) and throughput-bound beyond (recursive wins).  Measured
+// crossover (ms, right-looking / recursive): 3x4096 (W = 3 2^24) 3.17 / 3.37,
+// 4x4096 (2^26) 3.78 / 3.75, 1x8192 (2^26) 6.43 / 6.60, 4x4096 + 20x1024
+// (1.08 2^26) 4.21 / 3.97, 6x4096 6.03 / 5.07 ... 8x4096 6.80 / 5.67,
+// 2x8192 10.8 / 9.2; one BERT-Large layer (0.54 2^26) 2.69 / 3.00.
+// PF_INV_RECURSIVE=0/1 forces one.
+constexpr double kRecursiveFromW = 67108864.0;  // 2^26
 
 bool early_trtri_enabled() {  // PF_EARLY_TRTRI=0: whole TRTRI after the factorisation (A/B)
     static const bool on = [] {
@@ -1184,14 +1188,21 @@ bool early_trtri_enabled() {  // PF_EARLY_TRTRI=0: whole TRTRI after the factori
         return !(e && e[0] == '0');
     }();
     return on;
-}  // problems per call at which the recursive schedule takes over
+}
 
-bool use_recursive_inverse(int problems) {
+bool use_recursive_inverse(const std::vector<const pf_inverse_problem*>& probs) {
     static const int forced = [] {
         const char* e = std::getenv("PF_INV_RECURSIVE");
         return e ? (e[0] == '1' ? 1 : 0) : -1;
     }();
-    return forced >= 0 ? forced == 1 : problems >= g_recursive_from;
+    if (forced >= 0) return forced == 1;
+    double w = 0.0, dmax = 1.0;
+    for (const pf_inverse_problem* p : probs) {
+        const double d = p->d;
+        w += d * d * d;
+        dmax = std::max(dmax, d);
+    }
+    return w / dmax > kRecursiveFromW;
 }
 
 void damped_inverse_group(const std::vector<const pf_inverse_problem*>& probs, Emitter& em, bool recursive) {
@@ -1290,13 +1301,13 @@ std::size_t put_bytes(std::vector<uint8_t>& buf, const V& v, std::size_t align) 
 }
 
 GraphProg* build_program(const std::vector<std::vector<const pf_inverse_problem*>>& groups, cudaStream_t st) {
-    int n_problems = 0;
-    for (const auto& g : groups) n_problems += static_cast<int>(g.size());
     std::vector<GemmDesc> gemms;
     std::vector<CUtensorMap> maps;
     std::vector<SliceJob> slice_jobs;
     std::vector<LeafArgs> leaf_jobs;
     std::vector<Damp2D> damp_jobs;
+    std::vector<const pf_inverse_problem*> all_probs;
+    for (const auto& g : groups) all_probs.insert(all_probs.end(), g.begin(), g.end());
     std::vector<GraphBuilder> chains(groups.size());
     for (std::size_t gi = 0; gi < groups.size(); ++gi) {
         GraphBuilder& b = chains[gi];
@@ -1305,7 +1316,7 @@ GraphProg* build_program(const std::vector<std::vector<const pf_inverse_problem*
         b.slice_jobs = &slice_jobs;
         b.leaf_jobs = &leaf_jobs;
         b.damp_jobs = &damp_jobs;
-        damped_inverse_group(groups[gi], b, use_recursive_inverse(n_problems));
+        damped_inverse_group(groups[gi], b, use_recursive_inverse(all_probs));
     }
     // interleave the chains phase by phase: round r holds phase r of every
     // group, so a task only ever waits on lower-indexed tasks
@@ -1687,7 +1698,7 @@ int pf_damped_inverse_batched(const pf_inverse_problem* problems, int count, voi
             i = j;
         }
         const cudaStream_t st = static_cast<cudaStream_t>(stream);
-        const bool recursive = use_recursive_inverse(count);
+        const bool recursive = use_recursive_inverse(order);
         if (g_inverse_mode.load() == 1) {
             run_program(groups, st);  // one persistent launch for every group
         } else {
