@@ -211,6 +211,14 @@ struct SliceReq {
     Sliced dst;
 };
 
+bool warp_slice_2k() {  // PF_WARP_SLICE_2K=0: rows of 1025..2048 by the block-per-row kernel (A/B)
+    static const bool on = [] {
+        const char* e = std::getenv("PF_WARP_SLICE_2K");
+        return !(e && e[0] == '0');
+    }();
+    return on;
+}
+
 void launch_slices(const std::vector<SliceReq>& reqs, cudaStream_t st) {
     for (std::size_t i = 0; i < reqs.size(); i += kMaxSliceJobs) {
         SliceBatch b{};
@@ -223,11 +231,14 @@ void launch_slices(const std::vector<SliceReq>& reqs, cudaStream_t st) {
             rows = std::max(rows, r.dst.rows);
             kmax = std::max(kmax, r.dst.k);
         }
-        if (kmax > 1024 && kmax <= 4 * kLongThreads * kLongVec) {  // block per row, one pass
+        if (kmax > 1024 && kmax <= 2048 && warp_slice_2k()) {  // warp per row, 16 float4 per lane
+            launch(slice_kernel<16>, dim3((rows + 7) / 8, cnt), dim3(256), 0, st, b);
+            after_launch("slice_kernel");
+        } else if (kmax > 1024 && kmax <= 4 * kLongThreads * kLongVec) {  // block per row, one pass
             launch(slice_long_kernel, dim3(rows, cnt), dim3(kLongThreads), 0, st, b);
             after_launch("slice_long_kernel");
         } else {
-            launch(slice_kernel, dim3((rows + 7) / 8, cnt), dim3(256), 0, st, b);
+            launch(slice_kernel<8>, dim3((rows + 7) / 8, cnt), dim3(256), 0, st, b);
             after_launch("slice_kernel");
         }
     }

@@ -156,6 +156,9 @@ __device__ __forceinline__ void slice4(const float4 v, RowScale rs, uint32_t (&P
 // move 4 elements per lane per access (float4 in, char4 out) with 4 accesses
 // in flight per lane.  Loads bypass L1 (ld.global.cg): in the persistent
 // inversion kernel the rows were written by other SMs moments earlier.
+// kV: float4 per lane held in registers by the one-pass path (rows up to
+// 128 kV elements); longer rows take two passes.
+template <int kV = 8>
 __device__ __forceinline__ void slice_row(const SliceJob& J, int r, int lane) {
     int lo, hi;
     valid_range(J, r, lo, hi);
@@ -164,16 +167,16 @@ __device__ __forceinline__ void slice_row(const SliceJob& J, int r, int lane) {
     const bool vec = ((reinterpret_cast<uintptr_t>(row + lo) & 15) == 0) && ((hi - lo) % 4 == 0) &&
                      ((reinterpret_cast<uintptr_t>(p0 + lo) & 3) == 0) && (J.plane_stride % 4 == 0);
     float m = 0.0f;
-    if (vec && hi - lo <= 1024) {
+    if (vec && hi - lo <= 128 * kV) {
         // short row (every inversion operand up to d = 1024): ONE pass over
         // global memory, the row stays in registers between max and digits
         const float4* r4 = reinterpret_cast<const float4*>(row + lo);
         const int n4 = (hi - lo) / 4;
-        float4 v[8];
+        float4 v[kV];
 #pragma unroll
-        for (int u = 0; u < 8; ++u) v[u] = (lane + 32 * u < n4) ? __ldcg(r4 + lane + 32 * u) : make_float4(0.f, 0.f, 0.f, 0.f);
+        for (int u = 0; u < kV; ++u) v[u] = (lane + 32 * u < n4) ? __ldcg(r4 + lane + 32 * u) : make_float4(0.f, 0.f, 0.f, 0.f);
 #pragma unroll
-        for (int u = 0; u < 8; ++u)
+        for (int u = 0; u < kV; ++u)
             m = fmaxf(m, fmaxf(fmaxf(fabsf(v[u].x), fabsf(v[u].y)), fmaxf(fabsf(v[u].z), fabsf(v[u].w))));
 #pragma unroll
         for (int o = 16; o > 0; o >>= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, o));
@@ -184,9 +187,9 @@ __device__ __forceinline__ void slice_row(const SliceJob& J, int r, int lane) {
         const RowScale rs = row_scale2(e);
         (void)sc;
         SqAcc sq;
+        unsigned long long sq64 = 0;  // <= 16 float4 per lane: < 2^62
 #pragma unroll
-        unsigned long long sq64 = 0;  // <= 8 float4 per lane: < 2^61
-        for (int u = 0; u < 8; ++u) {
+        for (int u = 0; u < kV; ++u) {
             const int c = lane + 32 * u;
             if (c >= n4) continue;
             uint32_t packed[4];
@@ -196,7 +199,6 @@ __device__ __forceinline__ void slice_row(const SliceJob& J, int r, int lane) {
                 *reinterpret_cast<uint32_t*>(p0 + lo + 4 * c + pl * J.plane_stride) = packed[pl];
         }
         sq.add_u64(sq64);
-#pragma unroll
         sq.warp_reduce();
         if (lane == 0) J.sqnorm[r] = sq.value();
         return;
@@ -310,8 +312,8 @@ __global__ void __launch_bounds__(kLongThreads) slice_long_kernel(const __grid_c
     if (t == 0) J.exps[r] = e;
     const RowScale rs = row_scale2(e);
     SqAcc sq;
-#pragma unroll
     unsigned long long sq64 = 0;  // <= 8 float4 per thread: < 2^61
+#pragma unroll
     for (int u = 0; u < kLongVec; ++u) {
         const int c = t + kLongThreads * u;
         if (c >= n4) continue;
@@ -333,13 +335,14 @@ __global__ void __launch_bounds__(kLongThreads) slice_long_kernel(const __grid_c
 }
 
 // one warp per row; grid (ceil(rows / 8), jobs)
+template <int kV>
 __global__ void __launch_bounds__(256) slice_kernel(const __grid_constant__ SliceBatch b) {
     const SliceJob& J = b.j[blockIdx.y];
     const int r = blockIdx.x * 8 + (threadIdx.x >> 5);
     ptx::grid_dep_wait();  // PDL: the rows are produced by the previous launch
     ptx::grid_dep_launch();
     if (r >= J.rows) return;
-    slice_row(J, r, threadIdx.x & 31);
+    slice_row<kV>(J, r, threadIdx.x & 31);
 }
 
 }  // namespace pf
