@@ -234,8 +234,10 @@ void launch_slices(const std::vector<SliceReq>& reqs, cudaStream_t st) {
         if (kmax > 1024 && kmax <= 2048 && warp_slice_2k()) {  // warp per row, 16 float4 per lane
             launch(slice_kernel<16>, dim3((rows + 7) / 8, cnt), dim3(256), 0, st, b);
             after_launch("slice_kernel");
+        } else if (kmax > 1024 && kmax <= 4 * 128 * kLongVec) {
+            launch(slice_long_kernel<128>, dim3(rows, cnt), dim3(128), 0, st, b);  // block of 128 per row
         } else if (kmax > 1024 && kmax <= 4 * kLongThreads * kLongVec) {  // block per row, one pass
-            launch(slice_long_kernel, dim3(rows, cnt), dim3(kLongThreads), 0, st, b);
+            launch(slice_long_kernel<kLongThreads>, dim3(rows, cnt), dim3(kLongThreads), 0, st, b);
             after_launch("slice_long_kernel");
         } else {
             launch(slice_kernel<8>, dim3((rows + 7) / 8, cnt), dim3(256), 0, st, b);

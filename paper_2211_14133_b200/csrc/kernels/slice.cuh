@@ -266,16 +266,20 @@ __device__ __forceinline__ void slice_row(const SliceJob& J, int r, int lane) {
 constexpr int kLongThreads = 256;
 constexpr int kLongVec = 8;  // float4 per thread -> rows up to 8192
 
+template <int kThreads = kLongThreads>
 __device__ __forceinline__ bool long_row_ok(const SliceJob& J, int r, int& lo, int& hi) {
     valid_range(J, r, lo, hi);
     const float* row = J.src + static_cast<int64_t>(r) * J.ld;
     int8_t* p0 = J.planes + static_cast<int64_t>(r) * J.kpad;
     return ((reinterpret_cast<uintptr_t>(row + lo) & 15) == 0) && ((hi - lo) % 4 == 0) &&
            ((reinterpret_cast<uintptr_t>(p0 + lo) & 3) == 0) && (J.plane_stride % 4 == 0) &&
-           hi - lo <= 4 * kLongThreads * kLongVec;
+           hi - lo <= 4 * kThreads * kLongVec;
 }
 
-__global__ void __launch_bounds__(kLongThreads) slice_long_kernel(const __grid_constant__ SliceBatch b) {
+// kThreads per row: 128 for rows up to 4096 (8 float4 per thread: the per-row
+// reductions amortised over twice the elements), 256 up to 8192.
+template <int kThreads>
+__global__ void __launch_bounds__(kThreads) slice_long_kernel(const __grid_constant__ SliceBatch b) {
     const SliceJob& J = b.j[blockIdx.y];
     const int r = blockIdx.x;
     ptx::grid_dep_wait();
@@ -283,19 +287,19 @@ __global__ void __launch_bounds__(kLongThreads) slice_long_kernel(const __grid_c
     if (r >= J.rows) return;
     const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
     int lo, hi;
-    if (!long_row_ok(J, r, lo, hi)) {  // unaligned / over-long rows: warp path
+    if (!long_row_ok<kThreads>(J, r, lo, hi)) {  // unaligned / over-long rows: warp path
         if (warp == 0) slice_row(J, r, lane);
         return;
     }
-    __shared__ float red_m[kLongThreads / 32];
-    __shared__ SqAcc red_s[kLongThreads / 32];
+    __shared__ float red_m[kThreads / 32];
+    __shared__ SqAcc red_s[kThreads / 32];
     const float4* r4 = reinterpret_cast<const float4*>(J.src + static_cast<int64_t>(r) * J.ld + lo);
     int8_t* p0 = J.planes + static_cast<int64_t>(r) * J.kpad + lo;
     const int n4 = (hi - lo) / 4;
     float4 v[kLongVec];
 #pragma unroll
     for (int u = 0; u < kLongVec; ++u)
-        v[u] = (t + kLongThreads * u < n4) ? __ldcg(r4 + t + kLongThreads * u) : make_float4(0.f, 0.f, 0.f, 0.f);
+        v[u] = (t + kThreads * u < n4) ? __ldcg(r4 + t + kThreads * u) : make_float4(0.f, 0.f, 0.f, 0.f);
     float m = 0.0f;
 #pragma unroll
     for (int u = 0; u < kLongVec; ++u)
@@ -306,7 +310,7 @@ __global__ void __launch_bounds__(kLongThreads) slice_long_kernel(const __grid_c
     __syncthreads();
     m = red_m[0];
 #pragma unroll
-    for (int w = 1; w < kLongThreads / 32; ++w) m = fmaxf(m, red_m[w]);
+    for (int w = 1; w < kThreads / 32; ++w) m = fmaxf(m, red_m[w]);
     int e = 0;
     if (m > 0.0f) frexpf(m, &e);
     if (t == 0) J.exps[r] = e;
@@ -315,7 +319,7 @@ __global__ void __launch_bounds__(kLongThreads) slice_long_kernel(const __grid_c
     unsigned long long sq64 = 0;  // <= 8 float4 per thread: < 2^61
 #pragma unroll
     for (int u = 0; u < kLongVec; ++u) {
-        const int c = t + kLongThreads * u;
+        const int c = t + kThreads * u;
         if (c >= n4) continue;
         uint32_t packed[4];
         slice4(v[u], rs, packed, sq64);
@@ -329,7 +333,7 @@ __global__ void __launch_bounds__(kLongThreads) slice_long_kernel(const __grid_c
     if (t == 0) {
         SqAcc tot;
 #pragma unroll
-        for (int w = 0; w < kLongThreads / 32; ++w) tot.add(red_s[w]);
+        for (int w = 0; w < kThreads / 32; ++w) tot.add(red_s[w]);
         J.sqnorm[r] = tot.value();
     }
 }
