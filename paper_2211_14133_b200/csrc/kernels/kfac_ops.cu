@@ -219,6 +219,14 @@ bool warp_slice_2k() {  // PF_WARP_SLICE_2K=0: rows of 1025..2048 by the block-p
     return on;
 }
 
+bool slice_short_enabled() {  // PF_SLICE_SHORT=0: rows <= 256 by the warp-per-row kernel (A/B)
+    static const bool on = [] {
+        const char* e = std::getenv("PF_SLICE_SHORT");
+        return !(e && e[0] == '0');
+    }();
+    return on;
+}
+
 void launch_slices(const std::vector<SliceReq>& reqs, cudaStream_t st) {
     for (std::size_t i = 0; i < reqs.size(); i += kMaxSliceJobs) {
         SliceBatch b{};
@@ -231,11 +239,21 @@ void launch_slices(const std::vector<SliceReq>& reqs, cudaStream_t st) {
             rows = std::max(rows, r.dst.rows);
             kmax = std::max(kmax, r.dst.k);
         }
-        if (kmax > 1024 && kmax <= 2048 && warp_slice_2k()) {  // warp per row, 16 float4 per lane
+        bool aligned = true;  // every row's valid range 16-byte aligned (ranges start at multiples of 128)
+        for (int j = 0; j < cnt; ++j) {
+            const SliceReq& r = reqs[i + j];
+            aligned = aligned && aligned16(r.src) && r.ld % 4 == 0 && r.dst.k % 4 == 0 && r.dst.kpad % 4 == 0 &&
+                      r.dst.plane_stride % 4 == 0 && aligned16(r.dst.planes);
+        }
+        if (kmax <= 256 && aligned && slice_short_enabled()) {  // 8 lanes per row
+            launch(slice_short_kernel<8, 8>, dim3((rows + 31) / 32, cnt), dim3(256), 0, st, b);
+            after_launch("slice_short_kernel");
+        } else if (kmax > 1024 && kmax <= 2048 && warp_slice_2k()) {  // warp per row, 16 float4 per lane
             launch(slice_kernel<16>, dim3((rows + 7) / 8, cnt), dim3(256), 0, st, b);
             after_launch("slice_kernel");
         } else if (kmax > 1024 && kmax <= 4 * 128 * kLongVec) {
             launch(slice_long_kernel<128>, dim3(rows, cnt), dim3(128), 0, st, b);  // block of 128 per row
+            after_launch("slice_long_kernel");
         } else if (kmax > 1024 && kmax <= 4 * kLongThreads * kLongVec) {  // block per row, one pass
             launch(slice_long_kernel<kLongThreads>, dim3(rows, cnt), dim3(kLongThreads), 0, st, b);
             after_launch("slice_long_kernel");

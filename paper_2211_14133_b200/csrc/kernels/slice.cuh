@@ -338,6 +338,64 @@ __global__ void __launch_bounds__(kThreads) slice_long_kernel(const __grid_const
     }
 }
 
+// Short rows (<= 256 floats, every job 16-byte aligned: checked by the
+// caller): eight lanes per row, 32 rows per 256-thread block, so the per-row
+// reductions take 3 shuffle steps over up to 8 float4 per lane instead of 5
+// over one (the 128-wide panel operands of the right-looking inversion).
+// Template: kLanes lanes per row holding up to kV float4 each (8 x 8: rows
+// <= 256; a 16 x 16 form for rows <= 1024 measured slower than a warp per
+// row: 110 registers).
+template <int kLanes, int kV>
+__global__ void __launch_bounds__(256) slice_short_kernel(const __grid_constant__ SliceBatch b) {
+    const SliceJob& J = b.j[blockIdx.y];
+    const int g = threadIdx.x & (kLanes - 1);                              // lane within the row group
+    const int r = blockIdx.x * (256 / kLanes) + threadIdx.x / kLanes;  // row
+    ptx::grid_dep_wait();
+    ptx::grid_dep_launch();
+    const bool live = r < J.rows;
+    int lo = 0, hi = 0;
+    if (live) valid_range(J, r, lo, hi);
+    const int n4 = live ? (hi - lo) / 4 : 0;
+    const float4* r4 = reinterpret_cast<const float4*>(J.src + static_cast<int64_t>(live ? r : 0) * J.ld + lo);
+    float4 v[kV];
+#pragma unroll
+    for (int u = 0; u < kV; ++u)
+        v[u] = (g + kLanes * u < n4) ? __ldcg(r4 + g + kLanes * u) : make_float4(0.f, 0.f, 0.f, 0.f);
+    float m = 0.0f;
+#pragma unroll
+    for (int u = 0; u < kV; ++u)
+        m = fmaxf(m, fmaxf(fmaxf(fabsf(v[u].x), fabsf(v[u].y)), fmaxf(fabsf(v[u].z), fabsf(v[u].w))));
+#pragma unroll
+    for (int o = kLanes / 2; o > 0; o >>= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, o));
+    int e = 0;
+    if (m > 0.0f) frexpf(m, &e);
+    const RowScale rs = row_scale2(e);
+    int8_t* p0 = J.planes + static_cast<int64_t>(live ? r : 0) * J.kpad + lo;
+    unsigned long long sq64 = 0;
+#pragma unroll
+    for (int u = 0; u < kV; ++u) {
+        const int c = g + kLanes * u;
+        if (c >= n4) continue;
+        uint32_t packed[4];
+        slice4(v[u], rs, packed, sq64);
+#pragma unroll
+        for (int pl = 0; pl < 4; ++pl) *reinterpret_cast<uint32_t*>(p0 + 4 * c + pl * J.plane_stride) = packed[pl];
+    }
+    SqAcc sq;
+    sq.add_u64(sq64);
+#pragma unroll
+    for (int o = kLanes / 2; o > 0; o >>= 1) {
+        SqAcc t;
+        t.lo = __shfl_xor_sync(0xffffffffu, sq.lo, o);
+        t.hi = __shfl_xor_sync(0xffffffffu, sq.hi, o);
+        sq.add(t);
+    }
+    if (live && g == 0) {
+        J.exps[r] = e;
+        J.sqnorm[r] = sq.value();
+    }
+}
+
 // one warp per row; grid (ceil(rows / 8), jobs)
 template <int kV>
 __global__ void __launch_bounds__(256) slice_kernel(const __grid_constant__ SliceBatch b) {

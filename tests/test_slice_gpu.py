@@ -60,6 +60,9 @@ def unpack(K, buf, rows, k):
 
 CASES = [
     (64, 101, "normal"),      # rows not 16-byte aligned: scalar warp path
+    (200, 128, "normal"),     # 8 lanes per row (rows <= 256)
+    (96, 256, "scaled"),      # 8 lanes per row, zero rows and sign flips
+    (40, 36, "normal"),       # 8 lanes per row, rows shorter than the group
     (300, 1024, "normal"),    # warp path, single pass
     (257, 1500, "scaled"),    # block-per-row path, zero rows, sign flips, huge/tiny row scales
     (96, 4096, "normal"),     # block-per-row path
