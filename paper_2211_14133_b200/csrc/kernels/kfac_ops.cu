@@ -935,7 +935,8 @@ void cholesky_blocked(const std::vector<InvWs>& ws, Emitter& em,
                       const std::function<void(int)>& after_leaf = nullptr) {
     const int d = ws.front().d;
     const int nb = (d + kLeaf - 1) / kLeaf;
-    // event ids (per group, 16 available): F fork, A/U/B rings of 2, END per side stream
+    // event ids (pool_event, 32 per group): F fork, A/U/B rings of 2, END per side stream;
+    // 29-30 are the early-TRTRI fork/done (damped_inverse_group)
     auto evA = [](int k) { return 1 + (k & 1); };
     auto evU = [](int k) { return 3 + (k & 1); };
     auto evB = [](int k) { return 5 + (k & 1); };
