@@ -327,6 +327,16 @@ int make_desc(const GemmSpec& s, GemmDesc& d, CUtensorMap* maps, int n_maps) {
 
 inline int desc_tiles(const GemmDesc& d) { return d.lower ? d.tiles_m * (d.tiles_m + 1) / 2 : d.tiles_m * d.tiles_n; }
 
+int sm_count();
+
+bool gemm_persist_enabled() {  // PF_GEMM_PERSIST=0: one CTA per tile for long-K launches too (A/B)
+    static const bool on = [] {
+        const char* e = std::getenv("PF_GEMM_PERSIST");
+        return !(e && e[0] == '0');
+    }();
+    return on;
+}
+
 template <int kFmt, int kN>
 void launch_gemms_n(const std::vector<GemmSpec>& specs_in, cudaStream_t stream) {
     using T = GemmTraits<kFmt, kN>;
@@ -367,6 +377,25 @@ void launch_gemms_n(const std::vector<GemmSpec>& specs_in, cudaStream_t stream) 
                 batch.interleave = 0;
         }
         if (tiles == 0) continue;
+        if constexpr (kFmt == kOZ8 && kN == kTile) {
+            // long-K launches with more tiles than SMs: persistent CTAs
+            int kmin = 1 << 30;
+            for (int q = 0; q < probs; ++q) kmin = std::min(kmin, batch.probs[q].k);
+            if (gemm_persist_enabled() && kmin > 512 && tiles > sm_count()) {
+                static std::once_flag once;
+                std::call_once(once, [] {
+                    check(cudaFuncSetAttribute(umma_gemm_persist_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                               T::kSmemBytes),
+                          "cudaFuncSetAttribute(gemm persist)");
+                });
+                static std::atomic<int> next_slot{0};
+                const int slot = next_slot.fetch_add(1) % kTicketSlots;
+                launch(umma_gemm_persist_kernel, dim3(std::min(tiles, sm_count())), dim3(kPersistThreads),
+                       T::kSmemBytes, stream, batch, slot);
+                after_launch("umma_gemm_persist_kernel");
+                continue;
+            }
+        }
         launch(kernel, dim3(tiles), dim3(T::kThreads), T::kSmemBytes, stream, batch);
         after_launch("umma_gemm_kernel");
     }

@@ -550,4 +550,205 @@ __global__ void __launch_bounds__(GemmTraits<kFmt, kN>::kThreads, GemmTraits<kFm
     if (warp == 0) ptx::tmem_dealloc<T::kTmemCols>(tmem);
 }
 
+// ---------------------------------------------------------------------------
+// Persistent form for long-K kOZ8 launches with more tiles than SMs: one CTA
+// per SM pulls tiles from an atomic ticket counter (dynamic balance for
+// unequal tiles: triangular k-ranges, mixed K).  Warp 0 lane 0 fetches the
+// next tile and keeps the TMA ring running into it while warps 2-9 run the
+// current tile's epilogue; warp 1 lane 0 starts the next tile's MMAs once the
+// epilogue warps have drained the accumulators (tmem_empty).  Tile ids reach
+// the MMA and epilogue warps through a 4-entry shared-memory queue.  The last
+// CTA to finish resets its launch's counter slot (slots rotate per launch).
+constexpr int kPersistThreads = 320;  // warp 0 TMA, warp 1 MMA, warps 2-9 epilogue
+constexpr int kTicketSlots = 512;
+__device__ unsigned int g_tickets[kTicketSlots * 2];  // {next tile, CTAs done} per slot
+
+__device__ __forceinline__ void tile_of(const GemmBatch& batch, int gt, int& p, int& tm, int& tn, int& kb0,
+                                        int& kb1) {
+    int lt;
+    p = 0;
+    if (batch.interleave) {
+        p = gt % batch.n_probs;
+        lt = gt / batch.n_probs;
+    } else {
+        while (p + 1 < batch.n_probs && batch.probs[p + 1].tile_begin <= gt) ++p;
+        lt = gt - batch.probs[p].tile_begin;
+    }
+    const GemmDesc& P = batch.probs[p];
+    map_tile(P, lt, tm, tn);
+    int k_begin = 0, k_end = P.k;
+    if (P.k_mode == K_FROM_ROW_TILE) k_begin = tm * kTile;
+    if (P.k_mode == K_FROM_COL_TILE) k_begin = tn * kTile;
+    if (P.k_mode == K_TO_ROW_TILE_END) k_end = min(P.k, (tm + 1) * kTile);
+    if (P.k_mode == K_TO_COL_TILE_END) k_end = min(P.k, (tn + 1) * kTile);
+    constexpr int kKB = GemmTraits<kOZ8>::kKBlock;
+    kb0 = k_begin / kKB;
+    kb1 = max(kb0, (k_end + kKB - 1) / kKB);
+}
+
+__global__ void __launch_bounds__(kPersistThreads, 1)
+    umma_gemm_persist_kernel(const __grid_constant__ GemmBatch batch, int slot) {
+    using T = GemmTraits<kOZ8>;
+    constexpr int kStages = T::kStages;
+    constexpr int kQ = 4;
+    extern __shared__ uint8_t smem_raw[];
+    uint8_t* smem = reinterpret_cast<uint8_t*>(
+        (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~static_cast<uintptr_t>(1023));
+    uint8_t* tail = smem + kStages * T::kStageBytes + T::kCPad;
+    uint64_t* full = reinterpret_cast<uint64_t*>(tail);
+    uint64_t* empty = full + kStages;
+    uint64_t* done = empty + kStages;
+    uint64_t* tmem_empty = done + 1;
+    uint64_t* tq_full = tmem_empty + 1;
+    uint64_t* tq_empty = tq_full + kQ;
+    int* tq = reinterpret_cast<int*>(tq_empty + kQ);
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tq + kQ);
+    float* col_scale = reinterpret_cast<float*>(tail + 256);
+    const int warp = threadIdx.x >> 5;
+    const uint32_t lane = threadIdx.x & 31;
+
+    if (threadIdx.x == 0) {
+        for (int s = 0; s < kStages; ++s) {
+            ptx::mbar_init(&full[s], 1);
+            ptx::mbar_init(&empty[s], 1);
+        }
+        ptx::mbar_init(done, 1);
+        ptx::mbar_init(tmem_empty, 8);  // one arrive per epilogue warp
+        for (int q = 0; q < kQ; ++q) {
+            ptx::mbar_init(&tq_full[q], 1);
+            ptx::mbar_init(&tq_empty[q], 9);  // MMA thread + 8 epilogue warps
+        }
+        ptx::fence_barrier_init();
+    }
+    if (warp == 0) ptx::tmem_alloc<T::kTmemCols>(tmem_slot);
+    ptx::grid_dep_wait();
+    ptx::tc_fence_before();
+    __syncthreads();
+    ptx::tc_fence_after();
+    const uint32_t tmem = *tmem_slot;
+
+    auto a_plane = [&](int s, int pl) { return smem + s * T::kStageBytes + pl * T::kPlaneBytes; };
+    auto b_plane = [&](int s, int pl) {
+        return smem + s * T::kStageBytes + T::kPlanes * T::kPlaneBytes + pl * T::kPlaneBytesB;
+    };
+    const int total = batch.total_tiles;
+    unsigned int* ctr = g_tickets + 2 * slot;
+
+    if (warp == 0) {
+        if (lane == 0) {  // ---------------- tile fetch + TMA producer
+            int s = 0;
+            uint32_t ph = 0;
+            for (int it = 0;; ++it) {
+                const int q = it % kQ;
+                ptx::mbar_wait(&tq_empty[q], ((it / kQ) & 1) ^ 1u);
+                const unsigned int t = atomicAdd(ctr, 1u);
+                const int gt = t < static_cast<unsigned int>(total) ? static_cast<int>(t) : -1;
+                tq[q] = gt;
+                ptx::mbar_arrive(&tq_full[q]);
+                if (gt < 0) break;
+                int p, tm, tn, kb0, kb1;
+                tile_of(batch, gt, p, tm, tn, kb0, kb1);
+                const GemmDesc& P = batch.probs[p];
+                for (int kb = kb0; kb < kb1; ++kb) {
+                    ptx::mbar_wait(&empty[s], ph ^ 1u);
+                    ptx::mbar_arrive_expect_tx(&full[s], T::kStageBytes);
+                    const int kc = kb * T::kKBlock;
+                    ptx::tma_load_3d(a_plane(s, 0), &batch.maps[P.a_map], &full[s], kc, tm * kTile, 0);
+                    ptx::tma_load_3d(b_plane(s, 0), &batch.maps[P.b_map], &full[s], kc, tn * kTile, 0);
+                    if (++s == kStages) {
+                        s = 0;
+                        ph ^= 1u;
+                    }
+                }
+            }
+            // every CTA has fetched its terminal ticket when the count reaches
+            // gridDim.x: the last one resets the slot for a later launch
+            if (atomicAdd(ctr + 1, 1u) == gridDim.x - 1) {
+                atomicExch(ctr, 0u);
+                atomicExch(ctr + 1, 0u);
+            }
+        }
+    } else if (warp == 1) {
+        if (lane == 0) {  // ---------------- MMA issuer
+            int s = 0;
+            uint32_t ph = 0;
+            for (int it = 0;; ++it) {
+                const int q = it % kQ;
+                ptx::mbar_wait(&tq_full[q], (it / kQ) & 1);
+                const int gt = tq[q];
+                ptx::mbar_arrive(&tq_empty[q]);
+                if (gt < 0) break;
+                int p, tm, tn, kb0, kb1;
+                tile_of(batch, gt, p, tm, tn, kb0, kb1);
+                if (it > 0) {  // accumulators drained by the previous tile's epilogue
+                    ptx::mbar_wait(tmem_empty, (it - 1) & 1);
+                    ptx::tc_fence_after();
+                }
+                uint32_t started = 0;
+                for (int kb = kb0; kb < kb1; ++kb) {
+                    ptx::mbar_wait(&full[s], ph);
+                    ptx::tc_fence_after();
+#pragma unroll
+                    for (int ks = 0; ks < T::kKSteps; ++ks) {
+                        const uint32_t off = ks * 32;
+#pragma unroll
+                        for (int g = 0; g < kDigits; ++g) {
+#pragma unroll
+                            for (int sa = 0; sa <= g; ++sa) {
+                                const int sb = g - sa;
+                                const uint64_t da = ptx::sw64_kmajor_desc(ptx::smem_u32(a_plane(s, sa)) + off);
+                                const uint64_t db = ptx::sw64_kmajor_desc(ptx::smem_u32(b_plane(s, sb)) + off);
+                                ptx::umma_i8(tmem + g * kTile, da, db, T::kIdesc, (started >> g) & 1u);
+                                started |= 1u << g;
+                            }
+                        }
+                    }
+                    ptx::umma_commit(&empty[s]);
+                    if (++s == kStages) {
+                        s = 0;
+                        ph ^= 1u;
+                    }
+                }
+                ptx::umma_commit(done);  // also fires at once for an empty k-range
+            }
+        }
+    } else {  // ---------------- epilogue warps 2-9
+        const int ew = warp & 3;           // TMEM lane quarter this warp may access
+        const int part = (warp - 2) >> 2;  // column half
+        const int et = static_cast<int>(threadIdx.x) - 64;
+        for (int it = 0;; ++it) {
+            const int q = it % kQ;
+            ptx::mbar_wait(&tq_full[q], (it / kQ) & 1);
+            const int gt = tq[q];
+            __syncwarp();
+            if (lane == 0) ptx::mbar_arrive(&tq_empty[q]);
+            if (gt < 0) break;
+            int p, tm, tn, kb0, kb1;
+            tile_of(batch, gt, p, tm, tn, kb0, kb1);
+            const GemmDesc& P = batch.probs[p];
+            asm volatile("bar.sync 1, 256;" ::: "memory");  // previous tile's col_scale readers done
+            if (et < kTile) {
+                const int c = tn * kTile + et;
+                col_scale[et] = c < P.cols ? ptx::pow2f(__ldcg(P.b_exp + c)) : 0.0f;
+            }
+            const int r = tm * kTile + ew * 32 + static_cast<int>(lane);
+            const EpiRow er = epi_row<kOZ8>(P, tm, tn, r);
+            asm volatile("bar.sync 1, 256;" ::: "memory");
+            ptx::mbar_wait(done, it & 1);
+            ptx::tc_fence_after();
+            __syncwarp();
+            constexpr int kChunks = kTile / 16 / 2;
+            epilogue_chunks<kOZ8>(P, tm, tn, tmem + (static_cast<uint32_t>(ew * 32) << 16), r, col_scale,
+                                  part * kChunks, (part + 1) * kChunks, kb1 > kb0, er);
+            ptx::tc_fence_before();
+            __syncwarp();
+            if (lane == 0) ptx::mbar_arrive(tmem_empty);
+        }
+    }
+    ptx::grid_dep_launch();
+    ptx::tc_fence_before();
+    __syncthreads();
+    if (warp == 0) ptx::tmem_dealloc<T::kTmemCols>(tmem);
+}
+
 }  // namespace pf
