@@ -493,7 +493,8 @@ def run_gpu_arm(args, rank, world, local_rank):
                  "unit": "TFLOP/s", "frac": achieved / pk["bf16_tflops_sustained"],
                  "traffic": prof.get("syrk"), "peak_source": f"{pk_kind} bf16_tflops_sustained"}
     # The dominant kernel (about half of all kernel time, profiles/r01) is the
-    # fp32-accurate digit GEMM, umma_gemm_kernel<kOZ8>: each fp32-equivalent
+    # fp32-accurate digit GEMM (kOZ8; the precondition's long-K launches run the
+    # persistent form, umma_gemm_persist_kernel): each fp32-equivalent
     # FLOP is 10 int8 tensor-core products (kind::i8, 2x the bf16 rate).  Its
     # rate is taken on the precondition phase (2 digit-GEMM launches + 2 small
     # slicing launches, CUDA events on the launching stream): int8 TOP/s
@@ -501,7 +502,7 @@ def run_gpu_arm(args, rank, world, local_rank):
     prec_ms = phases["precondition"]
     int8_achieved = 10 * prec_f / (prec_ms * 1e-3) / 1e12
     int8_peak = 2 * pk["bf16_tflops_sustained"]
-    roof = {"kernel": "umma_gemm_kernel<kOZ8> (fp32-accurate digit GEMM; precondition phase, 2 launches)",
+    roof = {"kernel": "umma_gemm_persist_kernel (kOZ8 fp32-accurate digit GEMM; precondition phase, 2 launches)",
             "bound": "tensor", "achieved": int8_achieved, "peak": int8_peak, "unit": "TOP/s (int8)",
             "frac": int8_achieved / int8_peak, "traffic": prof.get("digit"),
             "algorithmic": "10 int8 products x (2 d_out^2 d_in + 2 d_out d_in^2) per linear, 6 linears = 1.03 int8-POP",

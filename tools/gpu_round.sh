@@ -21,6 +21,6 @@ if [ "${SKIP_FULL:-0}" != 1 ]; then
   run timeout 600 ncu --profile-from-start off --set full --clock-control none --import-source on \
       -k regex:umma_gemm_kernel -s 0 -c 1 -o "$OUT/syrk" python tools/prof_phase.py curvature 1
   run timeout 900 ncu --profile-from-start off --set full --clock-control none --import-source on \
-      -k regex:umma_gemm_kernel -s 0 -c 1 -o "$OUT/prec" python tools/prof_phase.py precondition 1
+      -k regex:umma_gemm -s 0 -c 2 -o "$OUT/prec" python tools/prof_phase.py precondition 1
 fi
 echo finished >> "$OUT/log.txt"
