@@ -42,9 +42,17 @@ __device__ long long* g_probe;
         __syncthreads();                                                 \
         if (threadIdx.x == 0 && blockIdx.x == 0) g_probe[i] = clock64(); \
     } while (0)
+// no barrier: the calling thread's own progress (tid = thread that stamps)
+#define PF_STAMP_T(i, tid)                                                  \
+    do {                                                                    \
+        if (threadIdx.x == (tid) && blockIdx.x == 0) g_probe[i] = clock64(); \
+    } while (0)
 #else
 #define PF_STAMP(i) \
     do {            \
+    } while (0)
+#define PF_STAMP_T(i, tid) \
+    do {                   \
     } while (0)
 #endif
 
@@ -446,6 +454,7 @@ __device__ __forceinline__ void leaf_body(const LeafArgs& A, float* leaf_smem, b
         // ---- A: chol(p) || rest of U(p-1) + T_p
         if (warp == 0) {
             chol32(Ls, LT, rdiag, lbuf, c0, A.n, A.col0, bad);
+            PF_STAMP_T(20 + p, 0);
         } else if (p > 0) {
             // rest of U(p-1) + panel p-1's contribution to T_p (the later T_bi
             // get theirs on the idle warps of phase B)
@@ -462,6 +471,7 @@ __device__ __forceinline__ void leaf_body(const LeafArgs& A, float* leaf_smem, b
                     tpanel_tile(PT, Xs, Tb, p, p - 1, v / (8 * p), v % (8 * p));
                 }
             }
+            PF_STAMP_T(24 + p, 32);
         }
         __syncthreads();
         PF_STAMP(3 + 3 * p);

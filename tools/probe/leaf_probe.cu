@@ -42,6 +42,11 @@ int main() {
     long long prev = h[0];
     for (int i = 1; i < 20; ++i) if (h[i]) { printf("%-8s %7lld cycles\n", names[i], h[i] - prev); prev = h[i]; }
     printf("total    %7lld cycles\n", h[19] - h[0]);
+    // phase A split: warp 0's chol32 vs warp 1's share of the trailing/T work
+    const int a_start[4] = {2, 5, 8, 11};  // stamp index that precedes phase A of panel p
+    for (int p = 0; p < 4; ++p)
+        printf("p%dA: chol32 %6lld  other warps %6lld  phase %6lld cycles\n", p, h[20 + p] - h[a_start[p]],
+               p ? h[24 + p] - h[a_start[p]] : 0LL, h[3 + 3 * p] - h[a_start[p]]);
     // residual check on host
     std::vector<float> X(n * n); cudaMemcpy(X.data(), dx, n * n * 4, cudaMemcpyDeviceToHost);
     // L^-1 check: X A X^T = I
