@@ -202,7 +202,7 @@ def test_precondition_hand_case(K):
         K.precondition(g, torch.eye(3, device="cuda"), torch.tensor([[1 / 3]], device="cuda"))
 
 
-@pytest.mark.parametrize("d_out,d_in", [(4096, 1024), (1024, 4096)])
+@pytest.mark.parametrize("d_out,d_in", [(4096, 1024), (1024, 4096), (1000, 2504), (2300, 700)])
 def test_precondition_update_baseline_sizes(K, d_out, d_in):
     """Fused W -= eta B^-1 G A^-1 at BERT-Large FFN shapes vs an fp64 torch product."""
     torch.manual_seed(0)
@@ -218,6 +218,33 @@ def test_precondition_update_baseline_sizes(K, d_out, d_in):
     delta_got = (w2.double() - w.double())
     delta_want = want - w.double()
     assert float(torch.linalg.norm(delta_got - delta_want) / torch.linalg.norm(delta_want)) <= 1e-5
+
+
+def test_precondition_batched_mixed_long_k(K):
+    """One batched call mixing K = 1024 and K = 4096 products (the BERT-Large
+    layer mix, run by the persistent long-K GEMM with its tile queue) equals
+    the per-problem calls bit for bit and an fp64 product to 1e-5."""
+    torch.manual_seed(1)
+    shapes = [(1024, 1024), (1024, 1024), (4096, 1024), (1024, 4096)]
+    items, singles, wants = [], [], []
+    for d_out, d_in in shapes:
+        ai = torch.randn(d_in, d_in, device="cuda", dtype=torch.float64) / d_in ** 0.5
+        ai = (ai @ ai.T + 0.1 * torch.eye(d_in, device="cuda", dtype=torch.float64)).float()
+        bi = torch.randn(d_out, d_out, device="cuda", dtype=torch.float64) / d_out ** 0.5
+        bi = (bi @ bi.T + 0.1 * torch.eye(d_out, device="cuda", dtype=torch.float64)).float()
+        g = torch.randn(d_out, d_in, device="cuda")
+        w = 0.02 * torch.randn(d_out, d_in, device="cuda")
+        wants.append(-1e-3 * (bi.double() @ g.double() @ ai.double()))
+        a_s, b_s = K.slice_matrix(ai), K.slice_matrix(bi)
+        w1 = w.clone()
+        K.precondition_update_sliced([(w1, g, a_s, b_s, 1e-3)])
+        singles.append((w, w1))
+        items.append((w.clone(), g, a_s, b_s, 1e-3))
+    K.precondition_update_sliced(items)
+    for (w, w1), (w2, *_), want in zip(singles, items, wants):
+        assert torch.equal(w2, w1)
+        d = w2.double() - w.double()
+        assert float(torch.linalg.norm(d - want) / torch.linalg.norm(want)) <= 1e-5
 
 
 def test_ngd_step_matches_reference(K):
