@@ -461,17 +461,31 @@ __global__ void __launch_bounds__(256) damp_kernel(const __grid_constant__ DampB
     const bool vec = (s.ld_src % 4 == 0) && (s.ld_dst % 4 == 0) && ((reinterpret_cast<uintptr_t>(s.src) & 15) == 0) &&
                      ((reinterpret_cast<uintptr_t>(s.dst) & 15) == 0);
     if (vec) {
+        // four float4 per lane in flight per round (the rows are long: a
+        // one-load-per-iteration loop is latency-bound)
         const int n4 = (r + 4) / 4;  // float4 groups covering columns [0, r]
-        for (int c4 = lane; c4 < n4; c4 += 32) {
-            float4 v = __ldcg(reinterpret_cast<const float4*>(src) + c4);
-            if (c4 == r / 4) {
-                const int e = r % 4;
-                if (e == 0) v.x += s.damping;
-                if (e == 1) v.y += s.damping;
-                if (e == 2) v.z += s.damping;
-                if (e == 3) v.w += s.damping;
+        const float4* s4 = reinterpret_cast<const float4*>(src);
+        float4* d4 = reinterpret_cast<float4*>(dst);
+        for (int b = 0; b < n4; b += 128) {
+            float4 v[4];
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+                const int c4 = b + lane + 32 * u;
+                v[u] = c4 < n4 ? __ldcg(s4 + c4) : make_float4(0.f, 0.f, 0.f, 0.f);
             }
-            reinterpret_cast<float4*>(dst)[c4] = v;
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+                const int c4 = b + lane + 32 * u;
+                if (c4 >= n4) continue;
+                if (c4 == r / 4) {
+                    const int e = r % 4;
+                    if (e == 0) v[u].x += s.damping;
+                    if (e == 1) v[u].y += s.damping;
+                    if (e == 2) v[u].z += s.damping;
+                    if (e == 3) v[u].w += s.damping;
+                }
+                d4[c4] = v[u];
+            }
         }
     } else {
         for (int c = lane; c <= r; c += 32) dst[c] = __ldcg(src + c) + (c == r ? s.damping : 0.0f);
