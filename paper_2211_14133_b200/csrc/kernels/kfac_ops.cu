@@ -1173,7 +1173,8 @@ int tri_height(int n, std::vector<std::vector<TriNode>>& by_h, int o) {
     return h;
 }
 
-void trtri_emit_levels(const std::vector<InvWs>& ws, Emitter& em, const std::vector<std::vector<TriNode>>& by_h);
+void trtri_emit_levels(const std::vector<InvWs>& ws, Emitter& em, const std::vector<std::vector<TriNode>>& by_h,
+                       int phases = 3);
 
 // Bottom-up TRTRI of the diagonal range [o, o + n) (its node tree as built by
 // tri_height: the whole matrix for (0, d), a subtree otherwise), every level
@@ -1184,10 +1185,14 @@ void trtri_levels(const std::vector<InvWs>& ws, Emitter& em, int o, int n) {
     trtri_emit_levels(ws, em, by_h);
 }
 
-void trtri_emit_levels(const std::vector<InvWs>& ws, Emitter& em, const std::vector<std::vector<TriNode>>& by_h) {
+// phases: bit 0 = T^T = (L21 X11)^T into w.t, bit 1 = X21 = -X22 T (and X^T);
+// a node's phase 1 needs only L21 and X11, so it can run before X22 exists.
+void trtri_emit_levels(const std::vector<InvWs>& ws, Emitter& em, const std::vector<std::vector<TriNode>>& by_h,
+                       int phases) {
     for (const auto& level : by_h) {
         std::vector<SliceReq> sl;
         std::vector<GemmSpec> g;
+        if (phases & 1) {
         for (const InvWs& w : ws) {
             size_t off0 = 0, off1 = 0;
             for (const TriNode& nd : level) {
@@ -1214,6 +1219,8 @@ void trtri_emit_levels(const std::vector<InvWs>& ws, Emitter& em, const std::vec
         em.gemms(g);
         sl.clear();
         g.clear();
+        }
+        if (!(phases & 2)) continue;
         for (const InvWs& w : ws) {
             size_t off0 = 0, off1 = 0;
             for (const TriNode& nd : level) {
@@ -1256,6 +1263,14 @@ void trtri_emit_levels(const std::vector<InvWs>& ws, Emitter& em, const std::vec
 // 2x8192 10.8 / 9.2; one BERT-Large layer (0.54 2^26) 2.69 / 3.00.
 // PF_INV_RECURSIVE=0/1 forces one.
 constexpr double kRecursiveFromW = 67108864.0;  // 2^26
+
+bool early_root_enabled() {  // PF_EARLY_ROOT=0: the root's T = L21 X11 after the factorisation (A/B)
+    static const bool on = [] {
+        const char* e = std::getenv("PF_EARLY_ROOT");
+        return !(e && e[0] == '0');
+    }();
+    return on;
+}
 
 bool early_trtri_enabled() {  // PF_EARLY_TRTRI=0: whole TRTRI after the factorisation (A/B)
     static const bool on = [] {
@@ -1307,19 +1322,29 @@ void damped_inverse_group(const std::vector<const pf_inverse_problem*>& probs, E
         if (d > kLeaf) tri_height(n1, left, 0);
         constexpr int evF = 29, evT = 30, kTrtriStream = 3;
         const bool split = !left.empty() && early_trtri_enabled();
+        // The root's first phase, T = L21 X11, needs only L[n1:, 0:n1] (final
+        // once panel n1/128 - 1's TRSM is done) and X11: it follows the left
+        // subtree on the side stream, leaving only X21 = -X22 T after the
+        // right subtree.
+        const std::vector<std::vector<TriNode>> root{{TriNode{0, n1, d - n1}}};
+        // (emitted after leaf n1/128, i.e. after TRSM(n1/128 - 1) on the main
+        // stream, which writes the last block column of L21)
         cholesky_blocked(ws, em, [&](int k) {
-            if (!split || k != n1 / kLeaf - 1) return;
+            const bool at_left = split && k == n1 / kLeaf - 1;
+            const bool at_root = split && early_root_enabled() && k == n1 / kLeaf;
+            if (!at_left && !at_root) return;
             em.record(evF);
             em.on(kTrtriStream);
             em.wait(evF);
-            trtri_emit_levels(ws, em, left);
+            if (at_left) trtri_emit_levels(ws, em, left);
+            if (at_root) trtri_emit_levels(ws, em, root, 1);
             em.record(evT);
             em.on(0);
         });
         if (split) {
             em.wait(evT);  // s0 / s1 level slots are reused by the right subtree
             trtri_levels(ws, em, n1, d - n1);
-            trtri_emit_levels(ws, em, {{TriNode{0, n1, d - n1}}});
+            trtri_emit_levels(ws, em, root, early_root_enabled() ? 2 : 3);
         } else {
             trtri_levels(ws, em, 0, d);
         }
