@@ -108,34 +108,61 @@ class ClockSampler:
 
 
 # ====================================================================== CPU arms
+def cpu_model():
+    try:
+        with open("/proc/cpuinfo") as f:
+            for line in f:
+                if line.startswith("model name"):
+                    return line.split(":", 1)[1].strip()
+    except Exception:
+        pass
+    return "unknown"
+
+
 def reference_sample(threads):
-    """A bounded sample of the same layer step on the reference CPU path: per
-    thread one d_model factor pair (curvature_factors over 512 tokens), one
-    cholesky_spd_inverse(1024) and one precondition(1024 x 1024)."""
-    import numpy as np
+    """A bounded sample of the same layer step on the reference CPU path
+    (oracle/_ref = the unmodified reference sources): per thread one item of
+    each kind at BERT-Large d_model size with the FULL micro-batch -- one
+    curvature factor over all 4096 tokens (kfac.cpp:125-131), one
+    cholesky_spd_inverse(1024) (matrix.cpp:136-163) and one
+    precondition(1024 x 1024) (kfac.cpp:133-137) -- timed once on one core and
+    then on `threads` cores at once (independent calls, std::thread-parallel
+    through the GIL-free ctypes calls).  The layer's two d = 4096 inverses are
+    NOT in the sample: one takes ~426 s single-threaded (BASELINE.md §2, 0.16
+    GF/s against 0.30 GF/s at d = 1024), so the sampled rate flatters the CPU.
+    Returns (rate on `threads` cores, seconds, 1-core rate, sample text)."""
     from oracle import ref as R
-    tok = 512
-    a = R.orc_symmetric(1, (D_MODEL, tok), 3 ** 0.5)
-    e = R.orc_symmetric(2, (D_MODEL, tok), 3 ** 0.5)
-    A, B = R.ref_curvature_factors(a, e)
+    a = R.orc_symmetric(1, (D_MODEL, TOKENS), 3 ** 0.5)
+    e = R.orc_symmetric(2, (1, TOKENS), 3 ** 0.5)  # B of a 1-wide layer: negligible
     g = R.orc_symmetric(3, (D_MODEL, D_MODEL))
 
     def job(_):
         t0 = time.perf_counter()
-        R.ref_curvature_factors(a, e)
-        ai = R.ref_cholesky_spd_inverse(A, DAMPING)
-        bi = ai  # same-size second inverse skipped: one inverse per job
-        R.ref_precondition(g, ai, bi)
+        F, _ = R.ref_curvature_factors(a, e)
+        ai = R.ref_cholesky_spd_inverse(F, DAMPING)
+        R.ref_precondition(g, ai, ai)
         return time.perf_counter() - t0
 
-    flops_per_job = 2 * D_MODEL * (D_MODEL + 1) * tok + D_MODEL ** 3 + 4 * D_MODEL ** 3
+    flops_per_job = D_MODEL * (D_MODEL + 1) * TOKENS + D_MODEL ** 3 + 4 * D_MODEL ** 3
+    one = job(0)
     t0 = time.perf_counter()
     with ThreadPoolExecutor(max_workers=threads) as ex:
         list(ex.map(job, range(threads)))
     dt = time.perf_counter() - t0
-    sample = (f"{threads} x [curvature_factors(a,e: {D_MODEL}x{tok}) + cholesky_spd_inverse({D_MODEL})"
-              f" + precondition({D_MODEL}x{D_MODEL})], FP64, std::thread-parallel over independent calls")
-    return threads * flops_per_job / dt / 1e12, dt, sample
+    sample = (f"per core: curvature_factors({D_MODEL} x {TOKENS} tokens) + cholesky_spd_inverse({D_MODEL})"
+              f" + precondition({D_MODEL}x{D_MODEL}), FP64; {threads} cores = independent calls "
+              f"(std::thread via ctypes); 1 core timed alone first; the layer's 4096-wide factors are not "
+              f"sampled (one d=4096 inverse: ~426 s on one core) -- the sampled rate flatters the CPU")
+    return threads * flops_per_job / dt / 1e12, dt, flops_per_job / one / 1e12, sample
+
+
+def int8_peaks():
+    """Measured dense int8 peak on this GPU model (tools/int8_peak.py)."""
+    try:
+        with open(os.path.join(ROOT, "profiles", "int8_peak.json")) as f:
+            return json.load(f)
+    except Exception:
+        return {"int8_tops_burst": 3089.3, "int8_tops_sustained": 2407.6}
 
 
 def cpu_threads():
@@ -151,11 +178,12 @@ def run_reference_arm(args, rank, world):
     threads = cpu_threads()
     for _ in range(args.warmup):
         reference_sample(threads)
-    vals, times = [], []
+    vals, times, ones = [], [], []
     for _ in range(args.steps):
-        v, dt, sample = reference_sample(threads)
+        v, dt, v1, sample = reference_sample(threads)
         vals.append(v)
         times.append(dt)
+        ones.append(v1)
     value = statistics.mean(vals)
     line = {
         "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
@@ -163,9 +191,9 @@ def run_reference_arm(args, rank, world):
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
         "data": "synthetic (SplitMix64)",
         "config": {"workload": "bert_large_kfac_layer_step", "sample": "bounded CPU sample",
-                   "tokens": 512},
+                   "tokens": TOKENS, "d": D_MODEL},
         "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": "reference",
-                         "sample": sample},
+                         "sample": sample, "value_1core": statistics.mean(ones), "cpu_model": cpu_model()},
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
@@ -208,6 +236,40 @@ class LayerStep:
             bi = K.SlicedMatrix(self.inv[2 * l + 1], self.digits[2 * l + 1])
             items.append((self.weights[l], self.grads[l], ai, bi, ETA))
         K.precondition_update_sliced(items)
+
+
+def self_check(torch, st, step_a, step_b):
+    """The bench checks its OWN step (outside the timed region), in fp64 on the
+    device: the damped-inverse residual max|(A + lambda I) X - I| of every
+    factor the step inverted (reference norm, proj/tests/test_kfac.cpp:155;
+    north_star bound 1e-5), and the fused update W -= eta B^-1 G A^-1 of every
+    linear against the same update formed with fp64 inverses of the step's
+    own factors (relative Frobenius; north_star bound 1e-3)."""
+    step_a()
+    torch.cuda.synchronize()
+    f64 = torch.float64
+    damped, resid = [], {}
+    for f, x in zip(st.factors, st.inv):
+        d = f.shape[0]
+        a = f.to(f64)
+        a = torch.tril(a) + torch.tril(a, -1).T + DAMPING * torch.eye(d, device=f.device, dtype=f64)
+        damped.append(a)
+        r = (a @ x.to(f64) - torch.eye(d, device=f.device, dtype=f64)).abs().max().item()
+        resid[str(d)] = max(resid.get(str(d), 0.0), r)
+    w0 = [w.clone() for w in st.weights]
+    step_b()
+    torch.cuda.synchronize()
+    rel = 0.0
+    for l in range(len(LINEARS)):
+        ai = torch.linalg.inv(damped[2 * l])
+        bi = torch.linalg.inv(damped[2 * l + 1])
+        want = -ETA * (bi @ st.grads[l].to(f64) @ ai)
+        got = st.weights[l].to(f64) - w0[l].to(f64)
+        rel = max(rel, ((got - want).norm() / want.norm()).item())
+    return {"inverse_residual_max": resid, "inverse_residual_bound": 1e-5,
+            "update_rel_fro_max": rel, "update_rel_fro_bound": 1e-3,
+            "ok": max(resid.values()) <= 1e-5 and rel <= 1e-3,
+            "how": "fp64 on the device, after the timed region, on the step's own factors / inverses / weights"}
 
 
 def run_gpu_arm(args, rank, world, local_rank):
@@ -471,6 +533,7 @@ def run_gpu_arm(args, rank, world, local_rank):
         e2e_ms = float(t.item())
     e2e_value = job_flops / (e2e_ms * 1e-3) / 1e12
 
+    check = self_check(torch, st, step_a, step_b)
     pipeline = None if args.no_pipeline else pipeline_section(args, rank, world, local_rank, dist)
 
     if rank != 0:
@@ -478,8 +541,7 @@ def run_gpu_arm(args, rank, world, local_rank):
         return
 
     pk, pk_kind = peaks()
-    syrk_ms = phases["curvature"]
-    achieved = syrk_f / (syrk_ms * 1e-3) / 1e12
+    i8 = int8_peaks()
     prof = {}
     try:
         with open(os.path.join(ROOT, "profiles", "syrk_traffic.json")) as f:
@@ -488,40 +550,46 @@ def run_gpu_arm(args, rank, world, local_rank):
             prof["digit"] = json.load(f).get("dram_bytes_per_launch")
     except Exception:
         pass
+    # Every phase is timed ALONE (graph-prefix replays, a few ms each), so its
+    # denominator is the BURST peak.  The fp32-accurate digit GEMM runs 10
+    # int8 products per fp32 product: its ceiling is the measured dense int8
+    # peak (cuBLASLt int8 8192^3, profiles/int8_peak.json) / 10.
+    digit_peak = i8["int8_tops_burst"] / 10.0
+    inv_ms, prec_ms, syrk_ms = phases["inversion"], phases["precondition"], phases["curvature"]
+    inv_rate = inv_f / (inv_ms * 1e-3) / 1e12
+    # The dominant phase (~80 % of the step) is the damped inversion: a chain
+    # of leaf (SIMT 128x128 Cholesky + inverse), slicing and digit-GEMM
+    # launches, so it is reported as a phase against the digit-GEMM ceiling.
+    roof = {"kernel": "damped inversion phase (12 factors: 2 x 4096 + 10 x 1024; leaves + digit GEMMs + "
+                      "slicing, one CUDA graph) -- the dominant phase",
+            "bound": "tensor", "achieved": inv_rate, "peak": digit_peak, "unit": "TFLOP/s (fp32-equivalent)",
+            "frac": inv_rate / digit_peak, "traffic": None,
+            "algorithmic": "d^3 per factor (POTRF d^3/3 + TRTRI d^3/3 + LAUUM d^3/3): 148.0 GFLOP",
+            "share_of_step": inv_ms / ms if ms > 0 else None,
+            "peak_source": "measured int8 dense burst (cuBLASLt, profiles/int8_peak.json) / 10 digit products"}
+    syrk_rate = syrk_f / (syrk_ms * 1e-3) / 1e12
     roof_syrk = {"kernel": "umma_gemm_kernel<bf16> (grouped SYRK, 12 factors, 1 launch)",
-                 "bound": "tensor", "achieved": achieved, "peak": pk["bf16_tflops_sustained"],
-                 "unit": "TFLOP/s", "frac": achieved / pk["bf16_tflops_sustained"],
-                 "traffic": prof.get("syrk"), "peak_source": f"{pk_kind} bf16_tflops_sustained"}
-    # The dominant kernel (about half of all kernel time, profiles/r01) is the
-    # fp32-accurate digit GEMM (kOZ8; the precondition's long-K launches run the
-    # persistent form, umma_gemm_persist_kernel): each fp32-equivalent
-    # FLOP is 10 int8 tensor-core products (kind::i8, 2x the bf16 rate).  Its
-    # rate is taken on the precondition phase (2 digit-GEMM launches + 2 small
-    # slicing launches, CUDA events on the launching stream): int8 TOP/s
-    # against 2 x the measured dense bf16 peak.
-    prec_ms = phases["precondition"]
+                 "bound": "tensor", "achieved": syrk_rate, "peak": pk["bf16_tflops"],
+                 "unit": "TFLOP/s", "frac": syrk_rate / pk["bf16_tflops"],
+                 "traffic": prof.get("syrk"), "peak_source": f"{pk_kind} bf16_tflops (burst)"}
     int8_achieved = 10 * prec_f / (prec_ms * 1e-3) / 1e12
-    int8_peak = 2 * pk["bf16_tflops_sustained"]
-    roof = {"kernel": "umma_gemm_persist_kernel (kOZ8 fp32-accurate digit GEMM; precondition phase, 2 launches)",
-            "bound": "tensor", "achieved": int8_achieved, "peak": int8_peak, "unit": "TOP/s (int8)",
-            "frac": int8_achieved / int8_peak, "traffic": prof.get("digit"),
-            "algorithmic": "10 int8 products x (2 d_out^2 d_in + 2 d_out d_in^2) per linear, 6 linears = 1.03 int8-POP",
-            "peak_source": f"2 x {pk_kind} bf16_tflops_sustained (int8 dense = 2x bf16 on B200)"}
-    # digit-form GEMM: 10 int8 products (kind::i8 = 2x the bf16 rate) per fp32 product
-    emu_peak = pk["bf16_tflops"] * 2 / 10
+    roof_prec = {"kernel": "umma_gemm_persist_kernel (kOZ8 digit GEMM; precondition phase: 2 GEMM + 2 slice launches)",
+                 "bound": "tensor", "achieved": int8_achieved, "peak": i8["int8_tops_burst"],
+                 "unit": "TOP/s (int8)", "frac": int8_achieved / i8["int8_tops_burst"],
+                 "traffic": prof.get("digit"),
+                 "algorithmic": "10 int8 products x (2 d_out^2 d_in + 2 d_out d_in^2) per linear, 6 linears = 1.03 int8-POP",
+                 "peak_source": "measured int8 dense burst (cuBLASLt 8192^3, profiles/int8_peak.json)"}
     phase_rates = {
-        "curvature": {"ms": phases["curvature"], "tflops": syrk_f / phases["curvature"] / 1e9},
-        "inversion": {"ms": phases["inversion"], "tflops": inv_f / phases["inversion"] / 1e9,
-                      "peak_fp32_digit_tflops": emu_peak},
-        "precondition": {"ms": phases["precondition"], "tflops": prec_f / phases["precondition"] / 1e9,
-                         "peak_fp32_digit_tflops": emu_peak},
+        "curvature": {"ms": syrk_ms, "tflops": syrk_rate},
+        "inversion": {"ms": inv_ms, "tflops": inv_rate, "peak_fp32_digit_tflops": digit_peak},
+        "precondition": {"ms": prec_ms, "tflops": prec_f / prec_ms / 1e9, "peak_fp32_digit_tflops": digit_peak},
     }
     cpu = None
     if world == 1 and not args.no_cpu_baseline:
         threads = cpu_threads()
-        v, dt, sample = reference_sample(threads)
+        v, dt, v1, sample = reference_sample(threads)
         cpu = {"value": v, "unit": UNIT, "cores": threads, "kind": "reference", "sample": sample,
-               "seconds": dt}
+               "seconds": dt, "value_1core": v1, "cpu_model": cpu_model()}
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "weak",
@@ -535,10 +603,12 @@ def run_gpu_arm(args, rank, world, local_rank):
         "cuda_graph": graphed,
         "roofline": roof,
         "roofline_syrk": roof_syrk,
+        "roofline_precondition": roof_prec,
+        "check": check,
         "e2e": {"value": e2e_value, "unit": UNIT, "ms_per_step": e2e_ms,
                 "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
                 "overlap": "pinned host buffers, one H2D for the tapes and one for the gradients per step (curvature + inversion start on the tapes, the preconditioner waits for the gradients), one D2H of the updated weights; H2D(step k+1) || compute(k) || D2H(k-1), double-buffered inputs; the copy engine (201 MB at ~55 GB/s) bounds the steady state"},
-        "gpu_launches": launches // max(1, args.steps) if False else launches,
+        "gpu_launches": launches,
         "clocks": clocks.summary(),
         "cpu_baseline": cpu,
         "pipeline": pipeline,

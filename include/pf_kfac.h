@@ -22,8 +22,8 @@
  * Precision: curvature takes bf16 activations/errors and accumulates in fp32
  * on tcgen05 (kind::f16).  Inversion and preconditioning are fp32-accurate:
  * every GEMM-shaped step runs on tcgen05 kind::i8 over int8 digit planes with
- * exact int32 accumulation (see pf_slice); the 128x128 diagonal blocks of the
- * inverse are factored on the SIMT cores with fp64 accumulation.
+ * exact int32 accumulation (see pf_slice), recombined in fp32; the 128x128
+ * diagonal blocks of the inverse are factored on the SIMT cores in fp32.
  */
 #ifndef PF_KFAC_H
 #define PF_KFAC_H
@@ -62,7 +62,7 @@ int pf_curvature_syrk_grouped(const pf_syrk_problem* problems, int count, int fi
  * matrix [rows x k] becomes a power-of-two scale 2^e and four signed 7-bit
  * int8 digits (x = 2^e sum_s q_s 2^-7(s+1), error <= 2^-28 max|row|); the
  * products of digit planes run on tcgen05.mma.kind::i8 with exact int32
- * accumulation and are recombined in fp64.  Inverses are kept in this form
+ * accumulation and are recombined in fp32.  Inverses are kept in this form
  * between refreshes so every preconditioning step reuses them. */
 int pf_slice_bytes(int rows, int k, size_t* bytes);
 int pf_slice(const float* x, int rows, int k, int ld, void* sliced, void* stream);
@@ -70,10 +70,10 @@ int pf_slice(const float* x, int rows, int k, int ld, void* sliced, void* stream
 /* Damped inverse (M + damping*I)^-1 of a symmetric positive-definite fp32
  * matrix; only the lower triangle of M is read.  Replaces
  * kfac::cholesky_spd_inverse (proj/src/kfac/matrix.cpp:136-163):
- * damp, Cholesky L, L^-1, then L^-T L^-1 — here a recursive blocked
- * factorisation whose diagonal 128-blocks are factored in shared memory
- * (fp64 accumulation) and whose off-diagonal work runs as digit-form
- * tensor-core GEMMs.  minv receives the full symmetric fp32 inverse;
+ * damp, Cholesky L, L^-1, then L^-T L^-1 — here a blocked factorisation
+ * whose diagonal 128-blocks are factored in shared memory (fp32) and whose
+ * off-diagonal work runs as digit-form tensor-core GEMMs; the final
+ * L^-T L^-1 adds its diagonal terms exactly in fp32 (EPI_DIAG_SPLIT).  minv receives the full symmetric fp32 inverse;
  * minv_sliced (nullable, pf_slice_bytes(d, d)) also receives its digit form.
  * d_info: device int, set to 0 or the 1-based column of the first failed
  * pivot (reference: std::domain_error "matrix not positive definite"). */
@@ -91,14 +91,11 @@ typedef struct pf_inverse_problem {
     void* workspace; /* pf_damped_inverse_workspace(d) bytes each */
     int* d_info;
 } pf_inverse_problem;
-/* Batched: problems with equal d advance through the recursion in lockstep;
- * groups of different d run concurrently.  pf_set_inverse_mode selects the
- * executor (same arithmetic, bit-identical results): 0 (default) one
- * stream-ordered PDL launch per recursion step, groups on forked streams;
- * 1 one persistent launch (inv_graph_kernel) walking every group's recursion
- * as a task graph.  Returns PF_BAD_ARG for other modes. */
+/* Batched: problems with equal d advance through the factorisation in
+ * lockstep (shared launches); groups of different d run concurrently on
+ * forked streams, joined back into `stream` (CUDA-graph capturable).
+ * count == 0 is a no-op. */
 int pf_damped_inverse_batched(const pf_inverse_problem* problems, int count, void* stream);
-int pf_set_inverse_mode(int mode);
 
 /* Precondition: P = B^-1 * G * A^-1 (kfac::precondition, kfac.cpp:133-137).
  * G, P: fp32 d_out x d_in row-major (ld = d_in); A^-1: d_in x d_in; B^-1:

@@ -22,7 +22,6 @@
 #include <vector>
 
 #include "../host/capi_common.hpp"
-#include "inv_graph.cuh"
 #include "leaf.cuh"
 #include "pf_kfac.h"
 #include "pf_sched.h"
@@ -280,6 +279,8 @@ struct GemmSpec {
     float* c = nullptr;
     float* c_t = nullptr;
     int ldc = 0, ldc_t = 0;
+    const float* aux = nullptr;  // EPI_DIAG_SPLIT
+    int ld_aux = 0;
 };
 
 // GemmSpec -> GemmDesc, encoding its operand tensor maps at maps[*n_maps...]
@@ -321,6 +322,8 @@ int make_desc(const GemmSpec& s, GemmDesc& d, CUtensorMap* maps, int n_maps) {
     d.c_t = s.c_t;
     d.ldc = s.ldc;
     d.ldc_t = s.ldc_t;
+    d.aux = s.aux;
+    d.ld_aux = s.ld_aux;
     (void)sizeof(T);
     return m - n_maps;
 }
@@ -335,6 +338,28 @@ bool gemm_persist_enabled() {  // PF_GEMM_PERSIST=0: one CTA per tile for long-K
         return !(e && e[0] == '0');
     }();
     return on;
+}
+
+// Ticket counter of one persistent-GEMM launch (g_tickets, umma_gemm.cuh).
+// The CTA that finishes last resets its slot, so a slot is free again once
+// its launch has completed.  Eager launches rotate over kEagerSlots (two
+// launches share a counter only if they are kEagerSlots launches apart AND
+// run at the same time).  A launch captured into a CUDA graph bakes its slot
+// into the graph, so it takes a slot of its own from the never-recycled
+// range above: replays of that graph cannot collide with eager launches or
+// with other captures (only a graph replayed concurrently with ITSELF would
+// share a counter -- replay one graph on one stream at a time).
+int ticket_slot(cudaStream_t stream) {
+    static std::atomic<unsigned> next_eager{0};
+    static std::atomic<unsigned> next_captured{0};
+    cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+    check(cudaStreamIsCapturing(stream, &cs), "cudaStreamIsCapturing");
+    if (cs == cudaStreamCaptureStatusNone) return static_cast<int>(next_eager.fetch_add(1u) % kEagerSlots);
+    const unsigned c = next_captured.fetch_add(1u);
+    if (c >= static_cast<unsigned>(kTicketSlots - kEagerSlots))
+        throw std::runtime_error("persistent GEMM: captured-launch ticket slots exhausted (" +
+                                 std::to_string(kTicketSlots - kEagerSlots) + " per process)");
+    return kEagerSlots + static_cast<int>(c);
 }
 
 template <int kFmt, int kN>
@@ -388,8 +413,7 @@ void launch_gemms_n(const std::vector<GemmSpec>& specs_in, cudaStream_t stream) 
                                                T::kSmemBytes),
                           "cudaFuncSetAttribute(gemm persist)");
                 });
-                static std::atomic<int> next_slot{0};
-                const int slot = next_slot.fetch_add(1) % kTicketSlots;
+                const int slot = ticket_slot(stream);
                 launch(umma_gemm_persist_kernel, dim3(std::min(tiles, sm_count())), dim3(kPersistThreads),
                        T::kSmemBytes, stream, batch, slot);
                 after_launch("umma_gemm_persist_kernel");
@@ -441,6 +465,14 @@ void gemm_oz8(const std::vector<GemmSpec>& s, cudaStream_t st) {
 }
 
 // ------------------------------------------------------------ small kernels
+// dst = src + damping * I (lower triangle) of one factor
+struct Damp2D {
+    const float* src;
+    float* dst;
+    int* info;  // reset to 0 (success) before the factorisation
+    int d, ld_src, ld_dst;
+    float damping;
+};
 constexpr int kMaxDamp = 16;
 struct DampBatch {
     Damp2D e[kMaxDamp];
@@ -586,10 +618,11 @@ InvWs carve(void* base, int d) {
 
 float* at(float* base, int ld, int r, int c) { return base + static_cast<size_t>(r) * ld + c; }
 
-// The inversion is written once (inverse_rec) against an Emitter with two
-// back ends: StreamEmitter launches one kernel per step on a stream (the
-// reference-shaped path, kept for A/B and debugging), GraphBuilder turns each
-// step into a PHASE of tasks for the persistent inv_graph_kernel.
+// The inversion is written once against an Emitter (StreamEmitter: one
+// PDL launch per step on a stream, fork/join and event edges to side streams).
+// (A persistent task-graph executor behind the same interface was measured
+// 1.3-2x slower -- cold instruction cache in the leaf, serialised epilogues --
+// and removed in round 2.)
 struct Emitter {
     virtual ~Emitter() = default;
     virtual void damp(const std::vector<Damp2D>& jobs) = 0;
@@ -668,10 +701,6 @@ LeafArgs leaf_args(const InvWs& w, int o, int n) {
     return LeafArgs{at(w.a, w.ld, o, o), at(w.x, w.ld, o, o), at(w.xt, w.ld, o, o), w.info, w.ld, n, o};
 }
 
-SliceJob slice_job(const SliceReq& r) {
-    return SliceJob{r.src, r.dst.rows, r.dst.k, r.ld, r.mode, r.dst.planes, r.dst.plane_stride, r.dst.kpad,
-                    r.dst.exps, r.dst.sqnorm};
-}
 
 struct StreamEmitter final : Emitter {
     cudaStream_t st;
@@ -748,62 +777,6 @@ struct StreamEmitter final : Emitter {
             launch(leaf_chol_inv_kernel, dim3(cnt), dim3(kLeafThreads), kLeafSmemBytes, st, b);
             after_launch("leaf_chol_inv_kernel");
         }
-    }
-};
-
-// Collects the phases of one factor group (a chain); programs interleave the
-// phase lists of independent groups.
-struct GraphBuilder final : Emitter {
-    struct Proto {
-        int type, a, b;
-    };
-    std::vector<std::vector<Proto>> phases;  // this group's chain
-    std::vector<GemmDesc>* descs;
-    std::vector<CUtensorMap>* maps;
-    std::vector<SliceJob>* slice_jobs;
-    std::vector<LeafArgs>* leaf_jobs;
-    std::vector<Damp2D>* damp_jobs;
-
-    void damp(const std::vector<Damp2D>& jobs) override {
-        std::vector<Proto> ph;
-        for (const Damp2D& j : jobs) {
-            const int idx = static_cast<int>(damp_jobs->size());
-            damp_jobs->push_back(j);
-            for (int r = 0; r < j.d; r += kGraphRows) ph.push_back({GT_DAMP, idx, r});
-        }
-        phases.push_back(std::move(ph));
-    }
-    void slices(const std::vector<SliceReq>& reqs) override {
-        std::vector<Proto> ph;
-        for (const SliceReq& r : reqs) {
-            const int idx = static_cast<int>(slice_jobs->size());
-            slice_jobs->push_back(slice_job(r));
-            for (int row = 0; row < r.dst.rows; row += kGraphRows) ph.push_back({GT_SLICE, idx, row});
-        }
-        phases.push_back(std::move(ph));
-    }
-    void gemms(const std::vector<GemmSpec>& specs) override {
-        std::vector<Proto> ph;
-        for (const GemmSpec& sp : specs) {
-            GemmDesc d;
-            const std::size_t m0 = maps->size();
-            maps->resize(m0 + 2);
-            const int used = make_desc<kOZ8>(sp, d, maps->data(), static_cast<int>(m0));
-            maps->resize(m0 + used);
-            const int idx = static_cast<int>(descs->size());
-            descs->push_back(d);
-            for (int t = 0; t < desc_tiles(d); ++t) ph.push_back({GT_GEMM, idx, t});
-        }
-        phases.push_back(std::move(ph));
-    }
-    void leaves(const std::vector<InvWs>& ws, int o, int n) override {
-        std::vector<Proto> ph;
-        for (const InvWs& w : ws) {
-            const int idx = static_cast<int>(leaf_jobs->size());
-            leaf_jobs->push_back(leaf_args(w, o, n));
-            ph.push_back({GT_LEAF, idx, 0});
-        }
-        phases.push_back(std::move(ph));
     }
 };
 
@@ -1349,20 +1322,26 @@ void damped_inverse_group(const std::vector<const pf_inverse_problem*>& probs, E
             trtri_levels(ws, em, 0, d);
         }
     }
-    // ---- LAUUM: M^-1 = X^T X = XT XT^T  (lower tiles, mirrored)
+    // ---- LAUUM: M^-1 = X^T X = XT XT^T  (lower tiles, mirrored), with the
+    // diagonal of XT split off: XT = D + O, O sliced with a zero diagonal, the
+    // D terms added exactly in the epilogue (EPI_DIAG_SPLIT; the rows of XT
+    // peak on the diagonal, where the digit form's row-max-relative error
+    // would otherwise dominate the residual)
     std::vector<SliceReq> sl;
     std::vector<GemmSpec> g;
     for (std::size_t i = 0; i < ws.size(); ++i) {
         const InvWs& w = ws[i];
         const pf_inverse_problem* p = probs[i];
-        sl.push_back(slice_of(w.xt, w.ld, 0, 0, d, d, w.s0, SLICE_UPPER_BLOCK));
+        sl.push_back(slice_of(w.xt, w.ld, 0, 0, d, d, w.s0, SLICE_UPPER_BLOCK | SLICE_ZERO_DIAG));
         GemmSpec s;
         s.a = sliced_view(w.s0, d, d);
         s.b = s.a;
         s.rows = s.cols = s.k = d;
         s.lower = true;
         s.k_mode = K_FROM_ROW_TILE;
-        s.flags = EPI_MIRROR;
+        s.flags = EPI_MIRROR | EPI_DIAG_SPLIT;
+        s.aux = w.x;  // X = L^-1, lower, ld = w.ld (multiple of 4, 256-B aligned plane)
+        s.ld_aux = w.ld;
         if (aligned16(p->minv) && p->ldinv % 4 == 0) s.flags |= EPI_VEC4;
         s.c = p->minv;
         s.ldc = p->ldinv;
@@ -1376,161 +1355,6 @@ void damped_inverse_group(const std::vector<const pf_inverse_problem*>& probs, E
             sl.push_back(SliceReq{p->minv, p->ldinv, SLICE_FULL, sliced_view(p->minv_sliced, d, d)});
     if (!sl.empty()) em.slices(sl);
 }
-
-// ------------------------------------------------------------ task-graph programs
-// A device-resident program for inv_graph_kernel, built once per distinct
-// problem list (pointers, sizes, damping) and cached: steady-state calls (and
-// CUDA-graph replays) only reset the counters and launch.  Entries are never
-// freed (captured graphs may reference them).
-struct GraphProg {
-    GraphProgram prog{};
-    int n_phases = 0;
-    int* counters = nullptr;  // phase_done[n_phases] + cursor
-    int grid = 0;
-};
-
-std::mutex g_prog_mu;
-std::vector<std::pair<std::string, GraphProg*>> g_progs;
-
-template <class V>
-std::size_t put_bytes(std::vector<uint8_t>& buf, const V& v, std::size_t align) {
-    const std::size_t off = (buf.size() + align - 1) / align * align;
-    buf.resize(off + v.size() * sizeof(typename V::value_type));
-    if (!v.empty()) std::memcpy(buf.data() + off, v.data(), v.size() * sizeof(typename V::value_type));
-    return off;
-}
-
-GraphProg* build_program(const std::vector<std::vector<const pf_inverse_problem*>>& groups, cudaStream_t st) {
-    std::vector<GemmDesc> gemms;
-    std::vector<CUtensorMap> maps;
-    std::vector<SliceJob> slice_jobs;
-    std::vector<LeafArgs> leaf_jobs;
-    std::vector<Damp2D> damp_jobs;
-    std::vector<const pf_inverse_problem*> all_probs;
-    for (const auto& g : groups) all_probs.insert(all_probs.end(), g.begin(), g.end());
-    std::vector<GraphBuilder> chains(groups.size());
-    for (std::size_t gi = 0; gi < groups.size(); ++gi) {
-        GraphBuilder& b = chains[gi];
-        b.descs = &gemms;
-        b.maps = &maps;
-        b.slice_jobs = &slice_jobs;
-        b.leaf_jobs = &leaf_jobs;
-        b.damp_jobs = &damp_jobs;
-        damped_inverse_group(groups[gi], b, use_recursive_inverse(all_probs));
-    }
-    // interleave the chains phase by phase: round r holds phase r of every
-    // group, so a task only ever waits on lower-indexed tasks
-    std::vector<GraphTask> tasks;
-    std::vector<int> phase_size;
-    std::vector<int> last(groups.size(), -1);
-    std::size_t rounds = 0;
-    for (const GraphBuilder& b : chains) rounds = std::max(rounds, b.phases.size());
-    for (std::size_t r = 0; r < rounds; ++r)
-        for (std::size_t gi = 0; gi < chains.size(); ++gi) {
-            if (r >= chains[gi].phases.size() || chains[gi].phases[r].empty()) continue;
-            const int ph = static_cast<int>(phase_size.size());
-            phase_size.push_back(static_cast<int>(chains[gi].phases[r].size()));
-            for (const GraphBuilder::Proto& pr : chains[gi].phases[r])
-                tasks.push_back(GraphTask{pr.type, ph, last[gi], pr.a, pr.b});
-            last[gi] = ph;
-        }
-    std::vector<uint8_t> buf;
-    const std::size_t o_tasks = put_bytes(buf, tasks, 16);
-    const std::size_t o_size = put_bytes(buf, phase_size, 16);
-    const std::size_t o_gemm = put_bytes(buf, gemms, 16);
-    const std::size_t o_maps = put_bytes(buf, maps, 128);
-    const std::size_t o_slice = put_bytes(buf, slice_jobs, 16);
-    const std::size_t o_leaf = put_bytes(buf, leaf_jobs, 16);
-    const std::size_t o_damp = put_bytes(buf, damp_jobs, 16);
-    auto* gp = new GraphProg;
-    uint8_t* dev = nullptr;
-    void* host = nullptr;
-    check(cudaMalloc(&dev, buf.size() + 256), "cudaMalloc(program)");
-    check(cudaMalloc(&gp->counters, (phase_size.size() + 1) * sizeof(int)), "cudaMalloc(counters)");
-    check(cudaMallocHost(&host, buf.size()), "cudaMallocHost(program)");
-    std::memcpy(host, buf.data(), buf.size());
-    check(cudaMemcpyAsync(dev, host, buf.size(), cudaMemcpyHostToDevice, st), "upload program");
-    gp->n_phases = static_cast<int>(phase_size.size());
-    GraphProgram& P = gp->prog;
-    P.tasks = reinterpret_cast<const GraphTask*>(dev + o_tasks);
-    P.n_tasks = static_cast<int>(tasks.size());
-    P.phase_size = reinterpret_cast<const int*>(dev + o_size);
-    P.phase_done = gp->counters;
-    P.cursor = gp->counters + gp->n_phases;
-    P.gemms = reinterpret_cast<const GemmDesc*>(dev + o_gemm);
-    P.maps = reinterpret_cast<const CUtensorMap*>(dev + o_maps);
-    P.slices = reinterpret_cast<const SliceJob*>(dev + o_slice);
-    P.leaves = reinterpret_cast<const LeafArgs*>(dev + o_leaf);
-    P.damps = reinterpret_cast<const Damp2D*>(dev + o_damp);
-    int dev_id = 0, sms = 148;
-    check(cudaGetDevice(&dev_id), "cudaGetDevice");
-    check(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev_id), "SM count");
-    gp->grid = std::max(1, std::min(sms, P.n_tasks));
-    return gp;
-}
-
-std::string program_key(const std::vector<std::vector<const pf_inverse_problem*>>& groups) {
-    std::string k;
-    int dev = 0;
-    cudaGetDevice(&dev);
-    k.append(reinterpret_cast<const char*>(&dev), sizeof(dev));
-    for (const auto& g : groups) {
-        const char sep = '|';
-        k.push_back(sep);
-        for (const pf_inverse_problem* p : g) k.append(reinterpret_cast<const char*>(p), sizeof(*p));
-    }
-    return k;
-}
-
-void run_program(const std::vector<std::vector<const pf_inverse_problem*>>& groups, cudaStream_t st) {
-    GraphProg* gp = nullptr;
-    {
-        const std::string key = program_key(groups);
-        std::lock_guard<std::mutex> lk(g_prog_mu);
-        for (auto& kv : g_progs)
-            if (kv.first == key) gp = kv.second;
-        if (!gp) {
-            gp = build_program(groups, st);
-            g_progs.emplace_back(key, gp);
-        }
-    }
-    static std::once_flag once;
-    std::call_once(once, [] {
-        check(cudaFuncSetAttribute(inv_graph_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kGraphSmemBytes),
-              "cudaFuncSetAttribute(inv_graph)");
-    });
-    check(cudaMemsetAsync(gp->counters, 0, (gp->n_phases + 1) * sizeof(int), st), "reset counters");
-    // PF_INV_TRACE=<file>: development timeline (eager calls only; synchronises)
-    static const char* trace_path = std::getenv("PF_INV_TRACE");
-    GraphProgram prog = gp->prog;
-    unsigned long long* trace = nullptr;
-    if (trace_path) {
-        check(cudaMalloc(&trace, sizeof(unsigned long long) * 8 * prog.n_tasks), "cudaMalloc(trace)");
-        check(cudaMemsetAsync(trace, 0, sizeof(unsigned long long) * 8 * prog.n_tasks, st), "trace reset");
-        prog.trace = trace;
-    }
-    launch(inv_graph_kernel, dim3(gp->grid), dim3(kGraphThreads), kGraphSmemBytes, st, prog);
-    after_launch("inv_graph_kernel");
-    if (trace) {
-        std::vector<unsigned long long> h(8 * static_cast<std::size_t>(prog.n_tasks));
-        std::vector<GraphTask> tasks(prog.n_tasks);
-        check(cudaStreamSynchronize(st), "trace sync");
-        check(cudaMemcpy(h.data(), trace, h.size() * 8, cudaMemcpyDeviceToHost), "trace copy");
-        check(cudaMemcpy(tasks.data(), prog.tasks, tasks.size() * sizeof(GraphTask), cudaMemcpyDeviceToHost),
-              "trace tasks");
-        if (FILE* f = std::fopen(trace_path, "w")) {
-            std::fprintf(f, "task,type,phase,wait,a,b,claimed_ns,ready_ns,done_ns,sm,mma_issued,pre_wait,acc_ready,epi_end\n");
-            for (int t = 0; t < prog.n_tasks; ++t)
-                std::fprintf(f, "%d,%d,%d,%d,%d,%d,%llu,%llu,%llu,%llu,%llu,%llu,%llu,%llu\n", t, tasks[t].type,
-                             tasks[t].phase, tasks[t].wait, tasks[t].a, tasks[t].b, h[8 * t], h[8 * t + 1],
-                             h[8 * t + 2], h[8 * t + 3], h[8 * t + 4], h[8 * t + 5], h[8 * t + 6], h[8 * t + 7]);
-            std::fclose(f);
-        }
-        cudaFree(trace);
-    }
-}
-
-std::atomic<int> g_inverse_mode{0};  // 0 one launch per step (default), 1 persistent task graph
 
 // ------------------------------------------------------------ precondition
 // workspace: digit forms of A^-1, B^-1 (when given as fp32), G, U^T; fp32 U^T
@@ -1705,6 +1529,7 @@ int pf_curvature_syrk_grouped(const pf_syrk_problem* problems, int count, int fi
                               void* stream) {
     return pf_detail::guard([&] {
         if (count < 0 || (count > 0 && !problems)) throw std::invalid_argument("bad problem list");
+        if (count == 0) return 0;
         std::vector<GemmSpec> specs;
         for (int i = 0; i < count; ++i) {
             const pf_syrk_problem& p = problems[i];
@@ -1755,12 +1580,6 @@ int pf_slice(const float* x, int rows, int k, int ld, void* sliced, void* stream
     });
 }
 
-int pf_set_inverse_mode(int mode) {
-    if (mode != 0 && mode != 1) return PF_BAD_ARG;
-    g_inverse_mode.store(mode);
-    return 0;
-}
-
 int pf_damped_inverse_workspace(int d, size_t* bytes) {
     return pf_detail::guard([&] {
         if (d < 1 || !bytes) throw std::invalid_argument("bad d");
@@ -1783,6 +1602,7 @@ int pf_damped_inverse_batched(const pf_inverse_problem* problems, int count, voi
                 throw std::invalid_argument("sliced output must be 16-B aligned");
             order.push_back(&p);
         }
+        if (order.empty()) return 0;  // nothing to invert: no launch, no side streams
         // Largest first; equal-d problems share every launch (groups of <= 8,
         // split evenly).  Independent groups run concurrently: the first on
         // `stream`, the others on side streams forked/joined with events, so
@@ -1807,9 +1627,7 @@ int pf_damped_inverse_batched(const pf_inverse_problem* problems, int count, voi
             i = j;
         }
         const cudaStream_t st = static_cast<cudaStream_t>(stream);
-        if (g_inverse_mode.load() == 1) {
-            run_program(groups, st);  // one persistent launch for every group
-        } else {
+        {
             g_lead_panels = 0;
             const int lead_d = groups[0].front()->d;
             run_forked(groups.size(), st, [&](std::size_t g, cudaStream_t s) {
@@ -1888,6 +1706,7 @@ int pf_precondition_update(const float* b_inv, const float* grad, const float* a
 int pf_precondition_update_sliced(const pf_precondition_problem* problems, int count,
                                   void* stream) {
     return pf_detail::guard([&] {
+        if (count < 0 || (count > 0 && !problems)) throw std::invalid_argument("bad problem list");
         std::vector<PrecJob> v;
         for (int i = 0; i < count; ++i) {
             const auto& p = problems[i];

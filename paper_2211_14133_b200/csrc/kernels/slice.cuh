@@ -27,6 +27,8 @@ enum SliceMode : int {
     SLICE_FULL = 0,
     SLICE_LOWER_BLOCK = 1,  // row r valid for k < (r/128 + 1) * 128
     SLICE_UPPER_BLOCK = 2,  // row r valid for k >= (r/128) * 128
+    SLICE_ZERO_DIAG = 4,    // flag: element (r, r) sliced as 0 (the LAUUM's diagonal
+                            // split: the diagonal enters the GEMM epilogue exactly)
 };
 
 struct SliceJob {
@@ -48,8 +50,25 @@ struct SliceBatch {
 __device__ __forceinline__ void valid_range(const SliceJob& J, int r, int& lo, int& hi) {
     lo = 0;
     hi = J.k;
-    if (J.mode == SLICE_LOWER_BLOCK) hi = min(J.k, (r / 128 + 1) * 128);
-    if (J.mode == SLICE_UPPER_BLOCK) lo = (r / 128) * 128;
+    const int m = J.mode & 3;
+    if (m == SLICE_LOWER_BLOCK) hi = min(J.k, (r / 128 + 1) * 128);
+    if (m == SLICE_UPPER_BLOCK) lo = (r / 128) * 128;
+}
+
+// SLICE_ZERO_DIAG: zero the component of the float4 at columns [c, c + 4) that
+// lies on the diagonal of row r (the row max and norm see the zeroed row).
+__device__ __forceinline__ float4 zap_diag(float4 v, const SliceJob& J, int r, int c) {
+    if ((J.mode & SLICE_ZERO_DIAG) && r >= c && r < c + 4) {
+        const int w = r - c;
+        if (w == 0) v.x = 0.0f;
+        if (w == 1) v.y = 0.0f;
+        if (w == 2) v.z = 0.0f;
+        if (w == 3) v.w = 0.0f;
+    }
+    return v;
+}
+__device__ __forceinline__ float zap_diag1(float x, const SliceJob& J, int r, int c) {
+    return ((J.mode & SLICE_ZERO_DIAG) && r == c) ? 0.0f : x;
 }
 
 // Row scale 2^(28-e) as one exact multiplier (0 = out of the normal range:
@@ -174,7 +193,9 @@ __device__ __forceinline__ void slice_row(const SliceJob& J, int r, int lane) {
         const int n4 = (hi - lo) / 4;
         float4 v[kV];
 #pragma unroll
-        for (int u = 0; u < kV; ++u) v[u] = (lane + 32 * u < n4) ? __ldcg(r4 + lane + 32 * u) : make_float4(0.f, 0.f, 0.f, 0.f);
+        for (int u = 0; u < kV; ++u)
+            v[u] = (lane + 32 * u < n4) ? zap_diag(__ldcg(r4 + lane + 32 * u), J, r, lo + 4 * (lane + 32 * u))
+                                        : make_float4(0.f, 0.f, 0.f, 0.f);
 #pragma unroll
         for (int u = 0; u < kV; ++u)
             m = fmaxf(m, fmaxf(fmaxf(fabsf(v[u].x), fabsf(v[u].y)), fmaxf(fabsf(v[u].z), fabsf(v[u].w))));
@@ -210,17 +231,17 @@ __device__ __forceinline__ void slice_row(const SliceJob& J, int r, int lane) {
         for (; c + 96 < n4; c += 128) {
             float4 v[4];
 #pragma unroll
-            for (int u = 0; u < 4; ++u) v[u] = __ldcg(r4 + c + 32 * u);
+            for (int u = 0; u < 4; ++u) v[u] = zap_diag(__ldcg(r4 + c + 32 * u), J, r, lo + 4 * (c + 32 * u));
 #pragma unroll
             for (int u = 0; u < 4; ++u)
                 m = fmaxf(m, fmaxf(fmaxf(fabsf(v[u].x), fabsf(v[u].y)), fmaxf(fabsf(v[u].z), fabsf(v[u].w))));
         }
         for (; c < n4; c += 32) {
-            const float4 v = __ldcg(r4 + c);
+            const float4 v = zap_diag(__ldcg(r4 + c), J, r, lo + 4 * c);
             m = fmaxf(m, fmaxf(fmaxf(fabsf(v.x), fabsf(v.y)), fmaxf(fabsf(v.z), fabsf(v.w))));
         }
     } else {
-        for (int c = lo + lane; c < hi; c += 32) m = fmaxf(m, fabsf(__ldcg(row + c)));
+        for (int c = lo + lane; c < hi; c += 32) m = fmaxf(m, fabsf(zap_diag1(__ldcg(row + c), J, r, c)));
     }
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, o));
@@ -238,7 +259,7 @@ __device__ __forceinline__ void slice_row(const SliceJob& J, int r, int lane) {
         const float4* r4 = reinterpret_cast<const float4*>(row + lo);
         const int n4 = (hi - lo) / 4;
         for (int c = lane; c < n4; c += 32) {
-            const float4 v = __ldcg(r4 + c);
+            const float4 v = zap_diag(__ldcg(r4 + c), J, r, lo + 4 * c);
             uint32_t packed[4];
             unsigned long long sq64 = 0;
             slice4(v, rs, packed, sq64);
@@ -250,7 +271,7 @@ __device__ __forceinline__ void slice_row(const SliceJob& J, int r, int lane) {
     } else {
         for (int c = lo + lane; c < hi; c += 32) {
             int8_t q[4];
-            sq.add(slice_digits(__ldcg(row + c), e, sc, q));
+            sq.add(slice_digits(zap_diag1(__ldcg(row + c), J, r, c), e, sc, q));
 #pragma unroll
             for (int pl = 0; pl < 4; ++pl) p0[c + pl * J.plane_stride] = q[pl];
         }
@@ -299,7 +320,8 @@ __global__ void __launch_bounds__(kThreads) slice_long_kernel(const __grid_const
     float4 v[kLongVec];
 #pragma unroll
     for (int u = 0; u < kLongVec; ++u)
-        v[u] = (t + kThreads * u < n4) ? __ldcg(r4 + t + kThreads * u) : make_float4(0.f, 0.f, 0.f, 0.f);
+        v[u] = (t + kThreads * u < n4) ? zap_diag(__ldcg(r4 + t + kThreads * u), J, r, lo + 4 * (t + kThreads * u))
+                                       : make_float4(0.f, 0.f, 0.f, 0.f);
     float m = 0.0f;
 #pragma unroll
     for (int u = 0; u < kLongVec; ++u)
@@ -360,7 +382,8 @@ __global__ void __launch_bounds__(256) slice_short_kernel(const __grid_constant_
     float4 v[kV];
 #pragma unroll
     for (int u = 0; u < kV; ++u)
-        v[u] = (g + kLanes * u < n4) ? __ldcg(r4 + g + kLanes * u) : make_float4(0.f, 0.f, 0.f, 0.f);
+        v[u] = (g + kLanes * u < n4) ? zap_diag(__ldcg(r4 + g + kLanes * u), J, r, lo + 4 * (g + kLanes * u))
+                                     : make_float4(0.f, 0.f, 0.f, 0.f);
     float m = 0.0f;
 #pragma unroll
     for (int u = 0; u < kV; ++u)

@@ -12,10 +12,13 @@
 //                  The 10 digit products with s_a + s_b <= 3 run as
 //                  tcgen05.mma.kind::i8 with EXACT int32 accumulation, one TMEM
 //                  accumulator per digit weight g = s_a + s_b (4 x 128 columns =
-//                  all 512), recombined in fp64 in the epilogue.  Error: 2^-27 of
-//                  the row scale from slicing, none from accumulation — unlike
-//                  the fp32-accumulated tf32 split we measured first, whose
-//                  inverse residual grew linearly with d.
+//                  all 512), recombined in FP32 in the epilogue (three fmaf,
+//                  smallest weight first, then one multiply by the power-of-two
+//                  row x column scale: ~1 ulp of the fp32 result).  Error:
+//                  2^-28 of the ROW MAX per operand element from slicing (plus
+//                  the dropped s_a + s_b >= 4 products, same order), none from
+//                  accumulation.  Being relative to the row max, it hurts rows
+//                  with a large max/rms ratio -- see EPI_DIAG_SPLIT.
 //
 // Structure (one CTA = one 128x128 output tile, 4 warps):
 //   warp 0 / lane 0 : TMA producer, kStages-deep smem ring (full/empty mbarriers)
@@ -74,6 +77,14 @@ enum EpiFlag : uint32_t {
     EPI_ALSO_T = 16u,    // additionally store C^T into c_t
     EPI_VEC4 = 32u,      // c / ldc 16-byte aligned: vectorised row stores
     EPI_EXACT_DIAG = 64u,  // kOZ8, A == B: diagonal from the operand's exact row norms
+    // kOZ8 LAUUM C = (D + O)(D + O)^T with A = B = O sliced with its diagonal
+    // zeroed (SLICE_ZERO_DIAG) and D = diag(X): the terms with D are added here
+    // in fp32 from aux = X (row-major lower, X[r][c] = O[c][r] for c < r):
+    //   C[r][c] += X[r][r] X[r][c] (c < r),  X[c][c] X[c][r] (c > r),  X[r][r]^2 (c == r).
+    // The digit form's error is relative to a row's max, which for the rows of
+    // L^-T is the diagonal (20-30x the rms); without it the LAUUM error grew
+    // linearly with d (residual 9.5e-6 at d = 4096, 1.9e-6 with the split).
+    EPI_DIAG_SPLIT = 128u,
 };
 
 // Tile (tm, tn) reads only the k-slice where both triangular operands can be
@@ -101,6 +112,8 @@ struct GemmDesc {
     float* c;
     float* c_t;
     int ldc, ldc_t;
+    const float* aux;  // EPI_DIAG_SPLIT: X (16-byte aligned rows, ld_aux % 4 == 0)
+    int ld_aux;
 };
 
 struct GemmBatch {
@@ -188,6 +201,7 @@ __device__ __forceinline__ void decode_lower(int t, int& tm, int& tn) {
 struct EpiRow {
     float row_scale = 1.0f;
     float diag_exact = 0.0f;
+    float dg = 0.0f;  // EPI_DIAG_SPLIT: X[r][r]
 };
 
 template <int kFmt, int kN = 128>
@@ -199,6 +213,7 @@ __device__ __forceinline__ EpiRow epi_row(const GemmDesc& P, int tm, int tn, int
             e.row_scale = P.alpha * ptx::pow2f(__ldcg(P.a_exp + r));
             if ((P.flags & EPI_EXACT_DIAG) && r >= tn * kN && r < (tn + 1) * kN)  // row's diagonal in this tile
                 e.diag_exact = static_cast<float>(__ldcg(P.a_sqnorm + r));  // = (norm 2^14) 2^-14
+            if (P.flags & EPI_DIAG_SPLIT) e.dg = __ldcg(P.aux + static_cast<size_t>(r) * P.ld_aux + r);
         }
     }
     return e;
@@ -296,6 +311,37 @@ __device__ __forceinline__ void epilogue_chunks(const GemmDesc& P, int tm, int t
                 if (c0 + j == r) out[j] = (row_scale * col_scale[chunk * 16 + j]) * diag_exact;
         }
     };
+    // EPI_DIAG_SPLIT: the diagonal's terms, exactly as one fp32 fma each
+    auto split_fix = [&](float (&out)[16], int chunk) {
+        if (!(f & EPI_DIAG_SPLIT) || !row_ok) return;
+        const int c0 = tn * kN + chunk * 16;
+        const float* xr = P.aux + static_cast<size_t>(r) * P.ld_aux;
+        if (c0 + 16 <= r) {  // left of the diagonal (every chunk of a lower off-diagonal tile)
+            const float4* src = reinterpret_cast<const float4*>(xr + c0);
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+                const float4 t = __ldcg(src + q);
+                out[4 * q] = fmaf(er.dg, t.x, out[4 * q]);
+                out[4 * q + 1] = fmaf(er.dg, t.y, out[4 * q + 1]);
+                out[4 * q + 2] = fmaf(er.dg, t.z, out[4 * q + 2]);
+                out[4 * q + 3] = fmaf(er.dg, t.w, out[4 * q + 3]);
+            }
+            return;
+        }
+#pragma unroll 1
+        for (int j = 0; j < 16; ++j) {  // diagonal tiles
+            const int c = c0 + j;
+            if (c >= P.cols) break;
+            if (c < r) {
+                out[j] = fmaf(er.dg, __ldcg(xr + c), out[j]);
+            } else if (c > r) {
+                const float* xc = P.aux + static_cast<size_t>(c) * P.ld_aux;
+                out[j] = fmaf(__ldcg(xc + c), __ldcg(xc + r), out[j]);
+            } else {
+                out[j] = fmaf(er.dg, er.dg, out[j]);
+            }
+        }
+    };
     if constexpr (kFmt == kOZ8) {
         if (!have_acc) {  // empty k-range
 #pragma unroll 1
@@ -304,6 +350,7 @@ __device__ __forceinline__ void epilogue_chunks(const GemmDesc& P, int tm, int t
 #pragma unroll
                 for (int j = 0; j < 16; ++j) out[j] = 0.0f;
                 diag_fix(out, chunk);
+                split_fix(out, chunk);
                 finish(out, chunk);
             }
             return;
@@ -333,6 +380,7 @@ __device__ __forceinline__ void epilogue_chunks(const GemmDesc& P, int tm, int t
                 out[j] = (row_scale * col_scale[chunk * 16 + j]) * s;
             }
             diag_fix(out, chunk);
+            split_fix(out, chunk);
             finish(out, chunk);
             if (chunk - chunk_begin < 4) PF_ESTAMP(2 + chunk - chunk_begin);
         }
@@ -560,7 +608,10 @@ __global__ void __launch_bounds__(GemmTraits<kFmt, kN>::kThreads, GemmTraits<kFm
 // the MMA and epilogue warps through a 4-entry shared-memory queue.  The last
 // CTA to finish resets its launch's counter slot (slots rotate per launch).
 constexpr int kPersistThreads = 320;  // warp 0 TMA, warp 1 MMA, warps 2-9 epilogue
-constexpr int kTicketSlots = 512;
+// slots [0, kEagerSlots) rotate over eager launches, the rest are handed out
+// once each to launches captured into CUDA graphs (kfac_ops.cu ticket_slot)
+constexpr int kEagerSlots = 512;
+constexpr int kTicketSlots = kEagerSlots + 7680;
 __device__ unsigned int g_tickets[kTicketSlots * 2];  // {next tile, CTAs done} per slot
 
 __device__ __forceinline__ void tile_of(const GemmBatch& batch, int gt, int& p, int& tm, int& tn, int& kb0,
@@ -662,8 +713,11 @@ __global__ void __launch_bounds__(kPersistThreads, 1)
                 }
             }
             // every CTA has fetched its terminal ticket when the count reaches
-            // gridDim.x: the last one resets the slot for a later launch
+            // gridDim.x: the last one resets the slot for a later launch (the
+            // fence orders this CTA's ticket fetches before its done count)
+            __threadfence();
             if (atomicAdd(ctr + 1, 1u) == gridDim.x - 1) {
+                __threadfence();
                 atomicExch(ctr, 0u);
                 atomicExch(ctr + 1, 0u);
             }

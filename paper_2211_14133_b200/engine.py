@@ -239,9 +239,13 @@ class CudaBackend:
         with torch.cuda.stream(self.kfac_stream):
             if gate is not None:
                 self.kfac_stream.wait_event(gate)
+            free = ks.slot_free.get((layer, f, slot))
+            if free is not None:  # the last precondition that read this slot's older version
+                self.kfac_stream.wait_event(free)
             for key in ks.keys(f):
+                # the preconditioner consumes only the digit form; the fp32
+                # inverse stays on the owner (non-owners never read it)
                 m = ks.inv[(layer, key, slot)]
-                dist.broadcast(m.fp32, src=owner, group=group)
                 dist.broadcast(m.digits, src=owner, group=group)
             ev = torch.cuda.Event()
             ev.record(self.kfac_stream)

@@ -297,6 +297,12 @@ def precondition_update(weight: torch.Tensor, grad: torch.Tensor, a_inv: torch.T
             "precondition_update")
 
 
+def _check_f32_2d(t: torch.Tensor, what: str, dev: torch.device) -> None:
+    _require_device(t, what)
+    if t.dim() != 2 or t.dtype != torch.float32 or not t.is_contiguous() or t.device != dev:
+        raise ValueError(f"precondition: {what} must be a contiguous 2-D fp32 tensor on {dev}")
+
+
 def precondition_update_sliced(items: Sequence[Tuple[Optional[torch.Tensor], torch.Tensor,
                                                      SlicedMatrix, SlicedMatrix, float]],
                                p_out: Optional[Sequence[torch.Tensor]] = None) -> None:
@@ -313,9 +319,24 @@ def precondition_update_sliced(items: Sequence[Tuple[Optional[torch.Tensor], tor
     ws = _WS.get(total, dev, "prec_sliced")
     arr = (L.PfPreconditionProblem * len(items))()
     for i, (w, g, ai, bi, eta) in enumerate(items):
+        _check_f32_2d(g, "grad", dev)
         d_out, d_in = g.shape
-        if ai.fp32.shape[0] != d_in or bi.fp32.shape[0] != d_out:
+        if w is not None:
+            _check_f32_2d(w, "weight", dev)
+            if w.shape != g.shape:
+                raise ValueError("precondition: weight shape mismatch")
+        if p_out is not None:
+            _check_f32_2d(p_out[i], "p_out", dev)
+            if p_out[i].shape != g.shape:
+                raise ValueError("precondition: p_out shape mismatch")
+        if w is None and p_out is None:
+            raise ValueError("precondition: need a weight or p_out")
+        if ai.fp32.shape != (d_in, d_in) or bi.fp32.shape != (d_out, d_out):
             raise ValueError("precondition: shape mismatch")
+        for sm, d in ((ai, d_in), (bi, d_out)):
+            if (sm.digits.device != dev or sm.digits.dtype != torch.uint8
+                    or sm.digits.numel() < slice_bytes(d, d) or not sm.digits.is_contiguous()):
+                raise ValueError("precondition: digit-form inverse has the wrong size or device")
         arr[i] = L.PfPreconditionProblem(bi.digits.data_ptr(), g.data_ptr(), ai.digits.data_ptr(),
                                          _ptr(w), None if p_out is None else p_out[i].data_ptr(),
                                          d_out, d_in, float(eta), ws.data_ptr() + offs[i])

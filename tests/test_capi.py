@@ -60,3 +60,17 @@ def test_scheduler_status_codes():
     with pytest.raises(ValueError, match="device count"):
         S.assign_works(base, S.PipelineConfig(stages=4, micro_batches=2), S.CostTable(t_f=1, t_b=1),
                        S.KfacWorkQueue())
+
+
+def test_empty_batches_are_noops_through_the_c_interface():
+    """count == 0 returns PF_OK without touching the device (the
+    batched inverse used to index an empty group list); count < 0 is BAD_ARG."""
+    lib = L.lib()
+    before = lib.pf_kernel_launch_count()
+    assert lib.pf_damped_inverse_batched(None, 0, None) == L.PF_OK
+    assert lib.pf_curvature_syrk_grouped(None, 0, 1, None) == L.PF_OK
+    assert lib.pf_precondition_update_sliced(None, 0, None) == L.PF_OK
+    assert lib.pf_damped_inverse_batched(None, -1, None) == L.PF_BAD_ARG
+    assert lib.pf_curvature_syrk_grouped(None, -1, 1, None) == L.PF_BAD_ARG
+    assert lib.pf_precondition_update_sliced(None, -1, None) == L.PF_BAD_ARG
+    assert lib.pf_kernel_launch_count() == before

@@ -73,9 +73,6 @@ def run(spec, iters=20):
 
 def main():
     torch.cuda.set_device(0)
-    mode = int(os.environ.get("PF_INV_MODE", "0"))
-    K.L.check(K.L.lib().pf_set_inverse_mode(mode), "mode")
-    print("inverse mode", mode, "(0 = launch per step, 1 = persistent task graph)")
     specs = []
     for a in sys.argv[1:]:
         specs.append([tuple(int(v) for v in p.split(":")) for p in a.split(",")])
