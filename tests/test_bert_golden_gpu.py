@@ -6,15 +6,17 @@ tests/golden/make_bert_golden.py from oracle/_ref = the unmodified
 Per factor size d in {768, 1024, 3072, 4096} (BERT-Base / BERT-Large
 hidden and FFN widths, n = 4096 tokens = one 32 x 128 micro-batch):
   factor   the tcgen05 SYRK of the regenerated bf16 tape vs the reference's
-           curvature_factors (kfac.cpp:125-131):      rel. Frobenius <= 1e-5
-           (north_star bound 1e-3; what remains is fp32 accumulation);
+           curvature_factors (kfac.cpp:125-131):      rel. Frobenius <= 2e-5
+           (north_star bound 1e-3; measured 7-8.5e-6: the tensor core's fp32
+           accumulation over K = 4096 tokens);
   inverse  pf_damped_inverse of fp32(A) vs the reference's
            cholesky_spd_inverse(fp32(A), lambda) (matrix.cpp:136-163):
              lambda = 0.1   max|(A + lambda I) X - I| <= 3e-6 and
                             rel. Frobenius to the reference <= 1e-5
              lambda = 1e-3  (stress: kappa up to ~4e3 at d = n = 4096)
-                            max|(A + lambda I) X - I| <= INV_STRESS_RESIDUAL and
-                            rel. Frobenius <= 1e-3;
+                            max|(A + lambda I) X - I| <= 5e-5 and
+                            rel. Frobenius <= 1e-4 (measured at d = 4096:
+                            1.9e-5 and 3.7e-5; d <= 3072: <= 2.7e-6);
 Per linear (d_out, d_in) in {(768, 3072), (1024, 4096), (4096, 1024)}:
   precondition  B^-1 G A^-1 (kfac.cpp:133-137) with the lambda = 0.1
                 inverses: rel. Frobenius <= 1e-5, and the fused update
@@ -37,12 +39,12 @@ import make_bert_golden as G  # noqa: E402  (test infrastructure: input generato
 pytestmark = pytest.mark.gpu
 
 GOLDEN = os.path.join(ROOT, "tests", "golden", "kfac_bert.npz")
-FACTOR_TOL = 1e-5
+FACTOR_TOL = 2e-5
 INV_RESIDUAL = {0.1: 3e-6, 1e-3: None}
-INV_REL = {0.1: 1e-5, 1e-3: 1e-3}
+INV_REL = {0.1: 1e-5, 1e-3: 1e-4}
 # lambda = 1e-3: kappa(A + lambda I) ~ (4 + lambda) / lambda at d = n (the
-# Marchenko-Pastur edge touches 0); an fp32 inverse's residual is ~ kappa * d^(1/2) * eps.
-INV_STRESS_RESIDUAL = 5e-4
+# Marchenko-Pastur edge touches 0), so the fp32 residual grows ~kappa-fold.
+INV_STRESS_RESIDUAL = 5e-5
 PREC_TOL = 1e-5
 
 
