@@ -23,8 +23,6 @@
 
 #include "../host/capi_common.hpp"
 #include "leaf.cuh"
-#include "leaf_sweep.cuh"
-#include "chain.cuh"
 #include "pf_kfac.h"
 #include "pf_sched.h"
 #include "slice.cuh"
@@ -113,37 +111,6 @@ void launch(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaSt
     cfg.attrs = attr;
     cfg.numAttrs = na;
     check(cudaLaunchKernelEx(&cfg, kernel, std::forward<Args>(args)...), "cudaLaunchKernelEx");
-}
-
-// launch() plus a thread-block cluster of `cl` CTAs along x
-template <typename... KArgs, typename... Args>
-void launch_cluster(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t st, int cl,
-                    Args&&... args) {
-    cudaLaunchConfig_t cfg{};
-    cfg.gridDim = grid;
-    cfg.blockDim = block;
-    cfg.dynamicSmemBytes = smem;
-    cfg.stream = st;
-    cudaLaunchAttribute attr[3];
-    int na = 0;
-    attr[na].id = cudaLaunchAttributeClusterDimension;
-    attr[na].val.clusterDim.x = cl;
-    attr[na].val.clusterDim.y = 1;
-    attr[na].val.clusterDim.z = 1;
-    ++na;
-    if (pdl_enabled()) {
-        attr[na].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-        attr[na].val.programmaticStreamSerializationAllowed = 1;
-        ++na;
-    }
-    if (g_launch_prio != 0) {
-        attr[na].id = cudaLaunchAttributePriority;
-        attr[na].val.priority = g_launch_prio;
-        ++na;
-    }
-    cfg.attrs = attr;
-    cfg.numAttrs = na;
-    check(cudaLaunchKernelEx(&cfg, kernel, std::forward<Args>(args)...), "cudaLaunchKernelEx(cluster)");
 }
 
 inline int round_up(int x, int m) { return (x + m - 1) / m * m; }
@@ -662,8 +629,6 @@ struct Emitter {
     virtual void slices(const std::vector<SliceReq>& reqs) = 0;
     virtual void gemms(const std::vector<GemmSpec>& specs) = 0;
     virtual void leaves(const std::vector<InvWs>& ws, int o, int n) = 0;
-    // chain step of panel o (o >= 128): L tile A[o, o-128] X^T, diagonal update, leaf(o)
-    virtual void chain_leaves(const std::vector<InvWs>& ws, int o, int n) = 0;
     // work emitted between side_begin(k) and side_end(k) may run concurrently
     // with what follows on the main chain until side_join(k)
     virtual void side_begin(int) {}
@@ -693,8 +658,7 @@ bool lead_delay_enabled() {
     }();
     return on;
 }
-constexpr int kMarkGroup = 1000;
-constexpr int kChainEvT0 = 11;  // pool_event ids 11, 12: L column k final (cholesky_chain's TRSM(k))  // pool_event(kMarkGroup, panel): lead progress marks
+constexpr int kMarkGroup = 1000;  // pool_event(kMarkGroup, panel): lead progress marks
 thread_local int g_lead_panels = 0;  // panels marked by the lead group of the current call
 
 // Per-thread, per-device pool of (stream, done event) pairs for the side
@@ -731,33 +695,6 @@ cudaEvent_t pool_event(int group, int id) {
     if (v.size() <= i) v.resize(i + 1, nullptr);
     if (!v[i]) check(cudaEventCreateWithFlags(&v[i], cudaEventDisableTiming), "cudaEventCreate(pool)");
     return v[i];
-}
-
-// PF_CHAIN=0: the chain of the right-looking factorisation as five launches per
-// panel (leaf, slice X, TRSM, slice L, one-tile diagonal update) instead of one
-// cluster step (chain.cuh) (A/B).  PF_CHAIN_CL=2|4|8: CTAs per cluster.
-bool chain_enabled() {
-    static const bool on = [] {
-        const char* e = std::getenv("PF_CHAIN");
-        return !(e && e[0] == '0');
-    }();
-    return on;
-}
-int chain_cluster() {
-    static const int cl = [] {
-        const char* e = std::getenv("PF_CHAIN_CL");
-        const int v = e ? std::atoi(e) : 4;
-        return (v == 2 || v == 8) ? v : 4;
-    }();
-    return cl;
-}
-
-bool leaf_sweep_enabled() {  // PF_LEAF=sweep: the single-sweep leaf (leaf_sweep.cuh) instead of the four-panel one (A/B)
-    static const bool on = [] {
-        const char* e = std::getenv("PF_LEAF");
-        return e && std::string(e) == "sweep";
-    }();
-    return on;
 }
 
 LeafArgs leaf_args(const InvWs& w, int o, int n) {
@@ -832,51 +769,13 @@ struct StreamEmitter final : Emitter {
             check(cudaFuncSetAttribute(leaf_chol_inv_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                        kLeafSmemBytes),
                   "cudaFuncSetAttribute(leaf)");
-            check(cudaFuncSetAttribute(leaf_sweep_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                       kSweepSmemBytes),
-                  "cudaFuncSetAttribute(leaf sweep)");
         });
-        const bool sweep = leaf_sweep_enabled();
         for (std::size_t i = 0; i < ws.size(); i += kMaxLeafBatch) {
             LeafBatch b{};
             const int cnt = static_cast<int>(std::min<std::size_t>(kMaxLeafBatch, ws.size() - i));
             for (int j = 0; j < cnt; ++j) b.e[j] = leaf_args(ws[i + j], o, n);
-            if (sweep) {
-                launch(leaf_sweep_kernel, dim3(cnt), dim3(kSweepThreads), kSweepSmemBytes, st, b);
-                after_launch("leaf_sweep_kernel");
-            } else {
-                launch(leaf_chol_inv_kernel, dim3(cnt), dim3(kLeafThreads), kLeafSmemBytes, st, b);
-                after_launch("leaf_chol_inv_kernel");
-            }
-        }
-    }
-    template <int kCl>
-    void chain_launch(const std::vector<InvWs>& ws, int o, int n) {
-        static std::once_flag once;
-        std::call_once(once, [] {
-            check(cudaFuncSetAttribute(chain_leaf_kernel<kCl>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                       chain_smem_bytes<kCl>()),
-                  "cudaFuncSetAttribute(chain)");
-        });
-        for (std::size_t i = 0; i < ws.size(); i += kMaxLeafBatch) {
-            ChainBatch b{};
-            const int cnt = static_cast<int>(std::min<std::size_t>(kMaxLeafBatch, ws.size() - i));
-            for (int j = 0; j < cnt; ++j) {
-                const InvWs& w = ws[i + j];
-                b.e[j] = ChainArgs{at(w.x, w.ld, o - kLeaf, o - kLeaf), at(w.a, w.ld, o, o - kLeaf), at(w.a, w.ld, o, o),
-                                   leaf_args(w, o, n)};
-            }
-            launch_cluster(chain_leaf_kernel<kCl>, dim3(cnt * kCl), dim3(kLeafThreads), chain_smem_bytes<kCl>(), st,
-                           kCl, b);
-            after_launch("chain_leaf_kernel");
-        }
-    }
-    void chain_leaves(const std::vector<InvWs>& ws, int o, int n) override {
-        ScopedPrio sp(prio);
-        switch (chain_cluster()) {
-            case 2: chain_launch<2>(ws, o, n); break;
-            case 8: chain_launch<8>(ws, o, n); break;
-            default: chain_launch<4>(ws, o, n); break;
+            launch(leaf_chol_inv_kernel, dim3(cnt), dim3(kLeafThreads), kLeafSmemBytes, st, b);
+            after_launch("leaf_chol_inv_kernel");
         }
     }
 };
@@ -1173,141 +1072,6 @@ void cholesky_blocked(const std::vector<InvWs>& ws, Emitter& em,
     }
 }
 
-// Blocked right-looking Cholesky, chain form (default; PF_CHAIN=0 selects
-// cholesky_blocked).  The main stream carries only the chain steps
-//   leaf(0) -> chain(1) -> chain(2) -> ...      (chain.cuh: L tile, diagonal
-//                                                update and leaf in one launch)
-// and panel k's side work runs on side stream S(k % 2) once leaf(k) is done:
-//   slice X_kk; TRSM L[>k, k] = A[>k, k] X_kk^T; slice L;
-//   col  A[>k+1, k+1] -= L[>k+1, k] L[k+1, k]^T, slice it (the A panel of k+1) -> A
-//   BU   block column k+2                                                      -> U
-//   BR   the rest, columns >= k+3, lower                                       -> B
-// chain(k) needs A[k, k-1] (final after col(k-2): event A(k-1)) and A[k, k]
-// (final after BU(k-2): event U(k-2)), i.e. side work two panels back -- a
-// whole chain step of slack.  Event T(k) marks L's column k final (TRSM(k)).
-void cholesky_chain(const std::vector<InvWs>& ws, Emitter& em, const std::function<void(int)>& after_leaf) {
-    const int d = ws.front().d;
-    const int nb = (d + kLeaf - 1) / kLeaf;
-    auto evA = [](int k) { return 1 + (k & 1); };
-    auto evU = [](int k) { return 3 + (k & 1); };
-    auto evB = [](int k) { return 5 + (k & 1); };
-    auto evX = [](int k) { return 9 + (k & 1); };
-    constexpr int evEnd0 = 7;
-    auto update = [](const InvWs& w, const Sliced& a, const Sliced& b, int rows, int cols, int r, int c,
-                     bool lower) {
-        GemmSpec u;
-        u.a = a;
-        u.b = b;
-        u.rows = rows;
-        u.cols = cols;
-        u.k = kLeaf;
-        u.lower = lower;
-        u.alpha = -1.0f;
-        u.beta = 1.0f;
-        u.flags = EPI_VEC4;
-        u.c = at(w.a, w.ld, r, c);
-        u.ldc = w.ld;
-        return u;
-    };
-    std::vector<SliceReq> sl;
-    std::vector<GemmSpec> g;
-    if (nb > 1) {  // A panel of panel 0
-        for (const InvWs& w : ws) sl.push_back(slice_of(w.a, w.ld, kLeaf, 0, d - kLeaf, kLeaf, w.pa[0], SLICE_FULL));
-        em.slices(sl);
-    }
-    bool side_used[2] = {false, false};
-    for (int k = 0; k < nb; ++k) {
-        const int o = k * kLeaf;
-        em.mark_lead(k, nb);
-        if (k == 0) {
-            em.leaves(ws, 0, std::min(kLeaf, d));
-        } else {
-            if (k >= 2) {
-                em.wait(evA(k - 1));
-                em.wait(evU(k - 2));
-            }
-            em.chain_leaves(ws, o, std::min(kLeaf, d - o));
-        }
-        if (after_leaf) after_leaf(k);
-        if (k == nb - 1) break;
-        const int r0 = o + kLeaf, m = d - r0, slot = k % 3;
-        const int side = 1 + (k & 1);
-        em.record(evX(k));
-        em.on(side);
-        em.wait(evX(k));
-        side_used[side - 1] = true;
-        sl.clear();
-        g.clear();
-        for (const InvWs& w : ws) sl.push_back(slice_of(w.x, w.ld, o, o, kLeaf, kLeaf, w.px[slot], SLICE_FULL));
-        em.slices(sl);
-        if (k >= 1) em.wait(evA(k));  // A panel of k (col(k-1), the other side stream)
-        // ---- TRSM: L[r0:, k] = A[r0:, k] X_kk^T
-        for (const InvWs& w : ws) {
-            GemmSpec t;
-            t.a = sliced_view(w.pa[slot], m, kLeaf);
-            t.b = sliced_view(w.px[slot], kLeaf, kLeaf);
-            t.rows = m;
-            t.cols = kLeaf;
-            t.k = kLeaf;
-            t.flags = EPI_VEC4;
-            t.c = at(w.l, w.ld, r0, o);
-            t.ldc = w.ld;
-            g.push_back(t);
-        }
-        em.gemms(g);
-        g.clear();
-        em.record(kChainEvT0 + (k & 1));
-        if (m > kLeaf) {
-            sl.clear();
-            for (const InvWs& w : ws) sl.push_back(slice_of(w.l, w.ld, r0, o, m, kLeaf, w.pl[slot], SLICE_FULL));
-            em.slices(sl);
-            if (k >= 1) em.wait(evU(k - 1));  // BU(k-1) wrote block column k+1
-            const int nc = kLeaf, m2 = m - kLeaf;
-            // col: A[r0+128:, k+1] -= L[r0+128:, k] L[k+1, k]^T, then the A panel of k+1
-            for (const InvWs& w : ws) {
-                const Sliced lp = sliced_view(w.pl[slot], m, kLeaf);
-                g.push_back(update(w, rows_of(lp, kLeaf, m2), rows_of(lp, 0, nc), m2, nc, r0 + kLeaf, r0, false));
-            }
-            em.gemms(g);
-            g.clear();
-            sl.clear();
-            const int ns = (k + 1) % 3;
-            for (const InvWs& w : ws) sl.push_back(slice_of(w.a, w.ld, r0 + kLeaf, r0, m2, kLeaf, w.pa[ns], SLICE_FULL));
-            em.slices(sl);
-            em.record(evA(k + 1));
-            // BU: block column k+2 (rows >= k+2) -- BR(k-1) also wrote it
-            if (k >= 1) em.wait(evB(k - 1));
-            const int nc2 = std::min(kLeaf, m2);
-            for (const InvWs& w : ws) {
-                const Sliced lb = rows_of(sliced_view(w.pl[slot], m, kLeaf), kLeaf, m2);
-                g.push_back(update(w, lb, rows_of(lb, 0, nc2), m2, nc2, r0 + kLeaf, r0 + kLeaf, false));
-            }
-            em.gemms(g);
-            g.clear();
-            em.record(evU(k));
-            // BR: columns >= k+3, lower
-            const int m3 = m2 - kLeaf;
-            if (m3 > 0) {
-                for (const InvWs& w : ws) {
-                    const Sliced lr = rows_of(sliced_view(w.pl[slot], m, kLeaf), 2 * kLeaf, m3);
-                    g.push_back(update(w, lr, lr, m3, m3, r0 + 2 * kLeaf, r0 + 2 * kLeaf, true));
-                }
-                em.gemms(g);
-                g.clear();
-            }
-            em.record(evB(k));
-        }
-        em.on(0);
-    }
-    for (int s = 0; s < 2; ++s) {
-        if (!side_used[s]) continue;
-        em.on(s + 1);
-        em.record(evEnd0 + s);
-        em.on(0);
-        em.wait(evEnd0 + s);
-    }
-}
-
 // X = L^-1 from the strictly-lower L (w.l) and the leaves' diagonal blocks:
 // per node X21 = -X22 (L21 X11); T^T = (L21 X11)^T needs only the left half,
 // so it runs on the depth's side stream while the right half is inverted.
@@ -1538,24 +1302,18 @@ void damped_inverse_group(const std::vector<const pf_inverse_problem*>& probs, E
         const std::vector<std::vector<TriNode>> root{{TriNode{0, n1, d - n1}}};
         // (emitted after leaf n1/128, i.e. after TRSM(n1/128 - 1) on the main
         // stream, which writes the last block column of L21)
-        const bool chain = chain_enabled();
-        auto hook = [&](int k) {
+        cholesky_blocked(ws, em, [&](int k) {
             const bool at_left = split && k == n1 / kLeaf - 1;
             const bool at_root = split && early_root_enabled() && k == n1 / kLeaf;
             if (!at_left && !at_root) return;
             em.record(evF);
             em.on(kTrtriStream);
             em.wait(evF);
-            if (chain && k >= 1) em.wait(kChainEvT0 + ((k - 1) & 1));  // L columns < k final (side TRSMs)
             if (at_left) trtri_emit_levels(ws, em, left);
             if (at_root) trtri_emit_levels(ws, em, root, 1);
             em.record(evT);
             em.on(0);
-        };
-        if (chain)
-            cholesky_chain(ws, em, hook);
-        else
-            cholesky_blocked(ws, em, hook);
+        });
         if (split) {
             em.wait(evT);  // s0 / s1 level slots are reused by the right subtree
             trtri_levels(ws, em, n1, d - n1);
@@ -1748,16 +1506,6 @@ extern "C" {
 
 int64_t pf_kernel_launch_count(void) { return g_launches.load(); }
 
-#ifdef PF_CHAIN_PROBE
-int pf_chain_probe_read(long long* out) {  // 64 records of 8; returns the record count
-    int n = 0;
-    if (cudaMemcpyFromSymbol(out, pf::g_chain_probe, sizeof(long long) * 64 * 8) != cudaSuccess) return -1;
-    if (cudaMemcpyFromSymbol(&n, pf::g_chain_probe_n, sizeof(int)) != cudaSuccess) return -1;
-    const int zero = 0;
-    cudaMemcpyToSymbol(pf::g_chain_probe_n, &zero, sizeof(int));
-    return n;
-}
-#endif
 #ifdef PF_GEMM_PROBE
 int pf_gemm_probe_read(long long* out) {  // 64 records of 8; returns the record count
     int n = 0;
