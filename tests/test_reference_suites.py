@@ -2,7 +2,7 @@
 code compiles against either implementation").
 
 tests/cpp/ref_compat/Makefile compiles /root/reference/proj/tests/
-test_schedule.cpp, test_bubblefill.cpp (doctest shim) and acceptance.cpp
+test_schedule.cpp, test_bubblefill.cpp, test_perfmodel.cpp (doctest shim) and acceptance.cpp
 criteria 1-6 in place, once against include/ + libpf_b200.so (ours_*) and
 once against the reference headers + the compiled reference (ref_*).  Both
 must pass with identical assertion counts."""
@@ -25,12 +25,12 @@ def run(name):
     return p.returncode, p.stdout + p.stderr
 
 
-@pytest.mark.parametrize("suite", ["test_schedule", "test_bubblefill"])
+@pytest.mark.parametrize("suite", ["test_schedule", "test_bubblefill", "test_perfmodel"])
 def test_reference_unit_tests_pass_against_this_library(suite):
     rc, out = run(f"ours_{suite}")
     assert rc == 0, out[-3000:]
     m = re.search(r"test cases: (\d+) \| (\d+) passed \| 0 failed; assertions: (\d+) \| 0 failed", out)
-    assert m and int(m.group(1)) >= 13 and int(m.group(3)) >= 700, out[-1000:]
+    assert m and int(m.group(1)) >= 13 and int(m.group(3)) >= 100, out[-1000:]
     rc_ref, out_ref = run(f"ref_{suite}")
     assert rc_ref == 0, out_ref[-3000:]
     # identical test cases and assertion counts on both implementations
