@@ -82,6 +82,17 @@ int pf_damped_inverse(const float* m, int d, int ldm, float damping, float* minv
                       void* minv_sliced, void* workspace, size_t workspace_bytes, int* d_info,
                       void* stream);
 
+/* Cholesky factor: L (lower, zeros above; ld = ldl) with L L^T = M + damping I
+ * for a symmetric positive-definite fp32 M (lower triangle read) -- replaces
+ * kfac::cholesky_factor (reference proj/src/kfac/matrix.cpp:117-134; damping
+ * 0 there).  The factorisation of pf_damped_inverse (128-column leaves on the
+ * SIMT cores, fp32-accurate int8-digit TRSM / trailing updates) without the
+ * triangular inverse and LAUUM.  Workspace: pf_damped_inverse_workspace(d).
+ * A pivot <= 0 or non-finite leaves its 1-based column in *d_info (the
+ * reference's std::domain_error), as pf_damped_inverse. */
+int pf_cholesky_factor(const float* m, int d, int ldm, float damping, float* l, int ldl, void* workspace,
+                       size_t workspace_bytes, int* d_info, void* stream);
+
 typedef struct pf_inverse_problem {
     const float* m;
     float* minv;

@@ -108,6 +108,8 @@ _SIGNATURES = {
     "pf_damped_inverse": (C.c_int, [C.c_void_p, C.c_int, C.c_int, C.c_float, C.c_void_p,
                                     C.c_int, C.c_void_p, C.c_void_p, C.c_size_t, C.c_void_p,
                                     C.c_void_p]),
+    "pf_cholesky_factor": (C.c_int, [C.c_void_p, C.c_int, C.c_int, C.c_float, C.c_void_p, C.c_int,
+                                     C.c_void_p, C.c_size_t, C.c_void_p, C.c_void_p]),
     "pf_slice_bytes": (C.c_int, [C.c_int, C.c_int, P(C.c_size_t)]),
     "pf_slice": (C.c_int, [C.c_void_p, C.c_int, C.c_int, C.c_int, C.c_void_p, C.c_void_p]),
     "pf_damped_inverse_batched": (C.c_int, [P(PfInverseProblem), C.c_int, C.c_void_p]),

@@ -299,23 +299,25 @@ Matrix kron(const Matrix& a, const Matrix& b) {
     return out;
 }
 
+// Reference matrix.cpp:117-134, on the GPU: pf_cholesky_factor (the damped
+// inverse's right-looking factorisation, fp32-accurate), damping 0.
 Matrix cholesky_factor(const Matrix& m) {
     require_square(m, "cholesky_factor");
     const int n = m.rows();
-    Matrix l(n, n);
-    for (int j = 0; j < n; ++j) {
-        double diag = m(j, j);
-        for (int k = 0; k < j; ++k) diag -= l(j, k) * l(j, k);
-        if (!(diag > 0.0) || !std::isfinite(diag))
-            throw std::domain_error("cholesky: matrix not positive definite (damping too small?)");
-        l(j, j) = std::sqrt(diag);
-        for (int i = j + 1; i < n; ++i) {
-            double s = m(i, j);
-            for (int k = 0; k < j; ++k) s -= l(i, k) * l(j, k);
-            l(i, j) = s / l(j, j);
-        }
-    }
-    return l;
+    if (n == 0) return Matrix();
+    require_device();
+    DevMat in(m), out(n, n);
+    std::size_t wsb = 0;
+    pf_check(pf_damped_inverse_workspace(n, &wsb), "cholesky workspace");
+    DevBuf ws(wsb), info(4);
+    pf_check(pf_cholesky_factor(in.f(), n, in.ld, 0.0f, out.f(), out.ld, ws.p, wsb, info.as<int>(), stream()),
+             "cholesky_factor");
+    int bad = 0;
+    sync();
+    cuda_check(cudaMemcpy(&bad, info.p, 4, cudaMemcpyDeviceToHost), "download info");
+    if (bad != 0)  // reference matrix.cpp:124-125
+        throw std::domain_error("cholesky: matrix not positive definite (damping too small?)");
+    return out.download();
 }
 
 std::vector<double> solve_spd(const Matrix& m, const std::vector<double>& rhs) {

@@ -532,6 +532,19 @@ __global__ void f32_to_bf16_kernel(const float* x, int64_t n, __nv_bfloat16* out
         out[i] = __float2bfloat16_rn(x[i]);
 }
 
+// pf_cholesky_factor: L = the leaves' diagonal blocks (already in `l`) + the
+// strictly-lower blocks of the right-looking factorisation (w.l), zeros above
+__global__ void assemble_l_kernel(const float* __restrict__ wl, int ldw, float* __restrict__ l, int ldl, int d) {
+    const int i = blockIdx.x;
+    const int diag0 = i / kLeaf * kLeaf;  // first column of row i's diagonal block
+    for (int j = threadIdx.x; j < d; j += blockDim.x) {
+        if (j > i)
+            l[static_cast<size_t>(i) * ldl + j] = 0.0f;
+        else if (j < diag0)
+            l[static_cast<size_t>(i) * ldl + j] = wl[static_cast<size_t>(i) * ldw + j];
+    }
+}
+
 // ------------------------------------------------------------ damped inverse
 // Workspace of one factor (ld = round_up(d, 4)):
 //   fp32  A (damped factor, updated in place), L (panel blocks L21),
@@ -554,6 +567,8 @@ struct InvWs {
     void* px[3] = {};
     void* pl[3] = {};
     int* info = nullptr;
+    float* lout = nullptr;  // pf_cholesky_factor: leaves also write their block of L here
+    int ldl = 0;
 };
 
 // n1 bound of the internal nodes, depth by depth (left child is the larger)
@@ -698,7 +713,12 @@ cudaEvent_t pool_event(int group, int id) {
 }
 
 LeafArgs leaf_args(const InvWs& w, int o, int n) {
-    return LeafArgs{at(w.a, w.ld, o, o), at(w.x, w.ld, o, o), at(w.xt, w.ld, o, o), w.info, w.ld, n, o};
+    LeafArgs a{at(w.a, w.ld, o, o), at(w.x, w.ld, o, o), at(w.xt, w.ld, o, o), w.info, w.ld, n, o};
+    if (w.lout) {
+        a.l = at(w.lout, w.ldl, o, o);
+        a.ldl = w.ldl;
+    }
+    return a;
 }
 
 
@@ -1654,6 +1674,28 @@ int pf_damped_inverse(const float* m, int d, int ldm, float damping, float* minv
         pf_inverse_problem p{m, minv, minv_sliced, d, ldm, ldinv, damping, workspace, d_info};
         const int rc = pf_damped_inverse_batched(&p, 1, stream);
         if (rc != 0) throw std::invalid_argument(pf_detail::last_error());
+        return 0;
+    });
+}
+
+int pf_cholesky_factor(const float* m, int d, int ldm, float damping, float* l, int ldl, void* workspace,
+                       size_t workspace_bytes, int* d_info, void* stream) {
+    return pf_detail::guard([&] {
+        if (d < 1 || ldm < d || ldl < d || !m || !l || !d_info || !workspace)
+            throw ShapeError("cholesky_factor: matrix not square / bad arguments");
+        if (workspace_bytes < inverse_ws_bytes(d)) throw std::invalid_argument("workspace too small");
+        if (!aligned16(workspace)) throw std::invalid_argument("workspace must be 16-B aligned");
+        const cudaStream_t st = static_cast<cudaStream_t>(stream);
+        InvWs w = carve(workspace, d);
+        w.info = d_info;
+        w.lout = l;
+        w.ldl = ldl;
+        g_lead_panels = 0;
+        StreamEmitter em(st, 0, true);
+        em.damp({Damp2D{m, w.a, d_info, d, ldm, w.ld, damping}});
+        cholesky_blocked({w}, em);
+        launch(assemble_l_kernel, dim3(d), dim3(256), 0, st, w.l, w.ld, l, ldl, d);
+        after_launch("assemble_l_kernel");
         return 0;
     });
 }

@@ -84,6 +84,8 @@ struct LeafArgs {
     int ld;    // shared leading dimension of a / x / xt
     int n;     // block size (<= 128; the tail block of a non-multiple-of-128 d)
     int col0;  // global column of the block (for info)
+    float* l = nullptr;  // optional: the block's Cholesky factor L_kk (lower part only; pf_cholesky_factor)
+    int ldl = 0;
 };
 
 struct LeafBatch {
@@ -418,6 +420,23 @@ __device__ __forceinline__ void report_bad(int* info, int bad) {
     }
 }
 
+// pf_cholesky_factor: the 32x32 diagonal block c0 of L from LT (LT[j][i] = L[i][j])
+__device__ __forceinline__ void store_l_diag(const float* LT, const LeafArgs& A, int c0) {
+    for (int idx = threadIdx.x; idx < 32 * 32; idx += kLeafThreads) {
+        const int i = idx >> 5, j = idx & 31;
+        if (j <= i && c0 + i < A.n) A.l[static_cast<size_t>(c0 + i) * A.ldl + c0 + j] = LT[j * kSmallPitch + i];
+    }
+}
+// ... and the panels below the diagonal blocks, PT_p[k][r] = L[r][32p + k]
+__device__ __forceinline__ void store_l_panels(const float* PT, const LeafArgs& A) {
+    for (int p = 0; p < 3; ++p)
+        for (int idx = threadIdx.x; idx < 32 * kLeaf; idx += kLeafThreads) {
+            const int r = idx >> 5, k = idx & 31;
+            if (r >= 32 * (p + 1) && r < A.n)
+                A.l[static_cast<size_t>(r) * A.ldl + 32 * p + k] = PT[p * kPTFloats + k * kXPitch + r];
+        }
+}
+
 // The whole leaf for one block, 256 threads, `leaf_smem` = kLeafSmemBytes of
 // 16-byte aligned shared memory.  `pdl`: called from a PDL-launched kernel.
 __device__ __forceinline__ void leaf_body(const LeafArgs& A, float* leaf_smem, bool pdl) {
@@ -475,6 +494,7 @@ __device__ __forceinline__ void leaf_body(const LeafArgs& A, float* leaf_smem, b
         }
         __syncthreads();
         PF_STAMP(3 + 3 * p);
+        if (A.l) store_l_diag(LT, A, c0);  // LT stays untouched until the next phase A
         if (p == 3) break;
         // ---- B: TRSM of the rows below || X_pp
         const int below = kLeaf - c0 - 32;
@@ -516,6 +536,7 @@ __device__ __forceinline__ void leaf_body(const LeafArgs& A, float* leaf_smem, b
     for (int t = tid; t < 192; t += kLeafThreads) xprod_tile(XTd, Tb, Xs, 3, t / 24, t % 24);
     __syncthreads();
     PF_STAMP(14);
+    if (A.l) store_l_panels(PT, A);
     if (pdl) ptx::grid_dep_launch();
     store_x(Xs, Ls, A.x, A.xt, A.ld, A.n);
     PF_STAMP(19);

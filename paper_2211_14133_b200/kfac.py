@@ -195,6 +195,38 @@ def damped_inverse_batched(mats: Sequence[torch.Tensor], damping: float,
     return outs
 
 
+def cholesky_factor(m: torch.Tensor, damping: float = 0.0, out: Optional[torch.Tensor] = None,
+                    check: bool = True) -> torch.Tensor:
+    """matrix.cpp:117-134: lower L with L L^T = M (+ damping I), zeros above,
+    on the GPU (pf_cholesky_factor: the damped inverse's factorisation).  Reads
+    the lower triangle of M.  A non-positive or non-finite pivot raises
+    NotPositiveDefinite with its 1-based column (the reference's
+    std::domain_error)."""
+    _require_device(m, "cholesky_factor")
+    if m.dim() != 2 or m.shape[0] != m.shape[1]:
+        raise ValueError("cholesky_factor: matrix not square")
+    if m.dtype != torch.float32 or m.stride(1) != 1:
+        raise ValueError("cholesky_factor: expects row-major fp32")
+    d = m.shape[0]
+    if out is None:
+        out = torch.empty((d, d), dtype=torch.float32, device=m.device)
+    elif out.shape != m.shape or out.dtype != torch.float32 or out.stride(1) != 1 or out.device != m.device:
+        raise ValueError("cholesky_factor: bad output buffer")
+    if d == 0:
+        return out
+    ws_bytes = inverse_workspace_bytes(d)
+    ws = _WS.get(ws_bytes, m.device, "inverse")
+    info = _WS.get(4, m.device, "info").view(torch.int32)[:1]
+    L.check(L.lib().pf_cholesky_factor(m.data_ptr(), d, m.stride(0), float(damping), out.data_ptr(),
+                                       out.stride(0), ws.data_ptr(), ws_bytes, info.data_ptr(), _stream()),
+            "cholesky_factor")
+    if check:
+        bad = int(info.cpu()[0])
+        if bad != 0:
+            raise NotPositiveDefinite(bad)
+    return out
+
+
 def block_diag_split_factor(m: torch.Tensor, k: int) -> List[torch.Tensor]:
     """kfac.cpp:203-218: the K diagonal blocks of a square factor (copies)."""
     if m.dim() != 2 or m.shape[0] != m.shape[1]:

@@ -150,6 +150,19 @@ int main() {
             CHECK(rel_fro(direct, dense) < 1e-5);
         }
     }
+    // ---- cholesky_factor on the GPU (matrix.cpp:117-134): hand case + non-PD
+    {
+        const Matrix l = cholesky_factor(Matrix{{4.0, 2.0}, {2.0, 3.0}});
+        CHECK(std::fabs(l(0, 0) - 2.0) < 1e-6 && std::fabs(l(1, 0) - 1.0) < 1e-6 &&
+              std::fabs(l(1, 1) - std::sqrt(2.0)) < 1e-6 && l(0, 1) == 0.0);
+        bool threw = false;
+        try {
+            (void)cholesky_factor(Matrix{{1.0, 2.0}, {2.0, 1.0}});
+        } catch (const std::domain_error&) {
+            threw = true;
+        }
+        CHECK(threw);
+    }
     // ---- ngd_step (test_kfac.cpp:275-330)
     {
         TinyMlp mlp{{Matrix{{2.0}}}, {Activation::Identity}, LossKind::MeanSquaredError};
