@@ -60,10 +60,25 @@ class StageKfac:
         return A_KEYS if f == 0 else E_KEYS
 
 
+_TRIL: Dict[Tuple[int, str], torch.Tensor] = {}
+
+
+def _tril_index(d: int, device) -> torch.Tensor:
+    """Flat row-major indices of the lower triangle of a d x d matrix (cached)."""
+    key = (d, str(device))
+    if key not in _TRIL:
+        r, c = torch.tril_indices(d, d, device=device)
+        _TRIL[key] = r * d + c
+    return _TRIL[key]
+
+
 class CudaBackend:
     def __init__(self, topo: R.Topology, bert: BertConfig, rank: int, device, kfac: bool = True,
-                 damping: float = 0.1, lr: float = 1e-3, seed: int = 0):
+                 damping: float = 0.1, lr: float = 1e-3, seed: int = 0, dist=None):
         cfg = topo.cfg
+        if dist is None:
+            import torch.distributed as dist
+        self.dist = dist  # torch.distributed, or the in-process stand-in of vdev.py
         self.topo, self.bert, self.rank, self.device, self.use_kfac = topo, bert, rank, device, kfac
         self.damping, self.lr = damping, lr
         self.B, self.Sq, L = cfg.micro_batch_size, cfg.seq_len, cfg.layers_per_stage
@@ -185,15 +200,25 @@ class CudaBackend:
             self._end("CURV", e0, self.kfac_stream, stage=st0, layer=l0, factor=f0, micro_batch=m0, items=len(items))
 
     def sync_curvature(self, stage, layer, f, group, gate):
+        """SyncCurvature (bubblefill.cpp:150-161): the replica average of one
+        layer's factor set.  The factors are lower-triangular (the SYRK writes
+        only the lower tiles), so only the packed lower triangles travel -- all
+        of the set's factors in ONE all-reduce of sum d(d+1)/2 floats, the
+        m_curv / 2 message the reference's cost model charges."""
         ks = self.kstate[stage]
         with torch.cuda.stream(self.kfac_stream):
             if gate is not None:
                 self.kfac_stream.wait_event(gate)
             e0 = self._begin(self.kfac_stream)
             if group is not None:
-                import torch.distributed as dist
-                for key in ks.keys(f):
-                    dist.all_reduce(ks.factor[(layer, key)], op=dist.ReduceOp.AVG, group=group)
+                mats = [ks.factor[(layer, key)] for key in ks.keys(f)]
+                idx = [_tril_index(m.shape[0], m.device) for m in mats]
+                packed = torch.cat([m.view(-1).index_select(0, i) for m, i in zip(mats, idx)])
+                self.dist.all_reduce(packed, op=self.dist.ReduceOp.AVG, group=group)
+                off = 0
+                for m, i in zip(mats, idx):
+                    m.view(-1).index_copy_(0, i, packed[off:off + i.numel()])
+                    off += i.numel()
             self._end("SYNC_CURV", e0, self.kfac_stream, stage=stage, layer=layer, factor=f)
 
     def invert(self, stage, layer, f, gate):
@@ -232,9 +257,10 @@ class CudaBackend:
 
     def broadcast_inverse(self, stage, layer, f, owner, group, gate):
         ks = self.kstate[stage]
-        import torch.distributed as dist
+        dist = self.dist
         if owner != self.rank:
             ks.version[(layer, f)] += 1
+            ks.started[(layer, f)] = False  # the next cycle's curvature starts a fresh factor here too
         slot = ks.version[(layer, f)] % 2
         with torch.cuda.stream(self.kfac_stream):
             if gate is not None:
@@ -254,7 +280,7 @@ class CudaBackend:
     def sync_grad(self, stage, group):
         if group is None:
             return
-        import torch.distributed as dist
+        dist = self.dist
         e0 = self._begin(self.compute)
         grads = [p.grad for p in self.stages[stage].parameters() if p.grad is not None]
         flat = torch.cat([g.reshape(-1) for g in grads])
@@ -449,7 +475,7 @@ class PipeFisherTrainer:
                 raise ValueError("costs: a CostTable or 'measured'")
             costs = self._measure_costs(damping, lr, seed, dist)
         self.costs = costs
-        self.backend = CudaBackend(self.topo, bert, rank, self.device, kfac, damping, lr, seed)
+        self.backend = CudaBackend(self.topo, bert, rank, self.device, kfac, damping, lr, seed, dist)
         self.filled = None
         if cfg.stages == 1 and cfg.replicas == 1:
             prog = R.inline_program(cfg, refresh)
@@ -459,7 +485,7 @@ class PipeFisherTrainer:
             base = S.build_schedule(cfg, costs)
             self.filled = S.assign_works(base, cfg, costs, S.enumerate_kfac_works(cfg, costs),
                                          S.AssignOptions(inversion_parallel=inversion_parallel))
-            progs = R.device_programs(self.filled, cfg, inversion_broadcast=inversion_parallel)
+            progs = R.device_programs(self.filled, cfg)  # inverse broadcast whenever W > 1
         if not kfac:
             progs = [[o for o in p if o.kind in (R.F_, R.B_, R.SYNC_GRAD, R.PREC)] for p in progs]
             for p in progs:
@@ -480,7 +506,7 @@ class PipeFisherTrainer:
         items on a throw-away backend, take the max over ranks (every rank
         must build the identical schedule), convert to the reference's
         cost-table semantics."""
-        probe = CudaBackend(self.topo, self.bert, self.rank, self.device, True, damping, lr, seed)
+        probe = CudaBackend(self.topo, self.bert, self.rank, self.device, True, damping, lr, seed, dist)
         t = measure_stage_times(probe)
         del probe
         torch.cuda.empty_cache()

@@ -56,13 +56,17 @@ def kernel_launches() -> int:
 
 
 class _Workspaces:
-    """Per-device scratch arena: grows, never shrinks; hot calls allocate nothing."""
+    """Scratch arena per (device, tag, stream): grows, never shrinks; hot calls
+    allocate nothing.  Keyed by the launching stream because calls on
+    different streams run concurrently (the K-FAC stream's inversions beside
+    the compute stream's preconditioning, one stream set per virtual device in
+    vdev.py); calls on one stream are ordered, so they can share."""
 
     def __init__(self):
-        self._bufs: Dict[Tuple[int, str], torch.Tensor] = {}
+        self._bufs: Dict[Tuple[int, str, int], torch.Tensor] = {}
 
     def get(self, nbytes: int, device: torch.device, tag: str = "ws") -> torch.Tensor:
-        key = (device.index or 0, tag)
+        key = (device.index or 0, tag, torch.cuda.current_stream(device).cuda_stream)
         buf = self._bufs.get(key)
         if buf is None or buf.numel() < nbytes:
             buf = torch.empty(max(nbytes, 256), dtype=torch.uint8, device=device)

@@ -127,10 +127,18 @@ def _channels_for(topo: Topology, dev: int, kind: str, stage: int, micro: int):
 
 
 def device_programs(filled: S.FilledSchedule, cfg: S.PipelineConfig,
-                    inversion_broadcast: bool = False) -> List[List[Op]]:
+                    inversion_broadcast: Optional[bool] = None) -> List[List[Op]]:
     """One refresh cycle (filled.refresh_period steps) of ops per device, in
     schedule-time order (ties by the reference's (start, kind) order; a
-    SyncGrad precedes the Precondition of its stage — A.6)."""
+    SyncGrad precedes the Precondition of its stage — A.6).
+
+    ``inversion_broadcast`` (default: whenever a stage has replicas): the
+    reference runs each (layer, factor) Inversion on ONE replica -- the front
+    one, or round-robin under inversion parallelism (bubblefill.cpp:162-173,
+    :277-285) -- and models no transfer (A.8); every other replica needs the
+    inverse, so the runtime broadcasts it from the inverting device."""
+    if inversion_broadcast is None:
+        inversion_broadcast = cfg.replicas > 1
     topo = Topology(cfg)
     nd = topo.n_devices()
     progs: List[List[Op]] = [[] for _ in range(nd)]
