@@ -279,7 +279,8 @@ struct GemmSpec {
     float* c = nullptr;
     float* c_t = nullptr;
     int ldc = 0, ldc_t = 0;
-    const float* aux = nullptr;  // EPI_DIAG_SPLIT
+    const float* aux = nullptr;  // EPI_DIAG_SPLIT: X and X^T
+    const float* aux_t = nullptr;
     int ld_aux = 0;
 };
 
@@ -323,6 +324,7 @@ int make_desc(const GemmSpec& s, GemmDesc& d, CUtensorMap* maps, int n_maps) {
     d.ldc = s.ldc;
     d.ldc_t = s.ldc_t;
     d.aux = s.aux;
+    d.aux_t = s.aux_t;
     d.ld_aux = s.ld_aux;
     (void)sizeof(T);
     return m - n_maps;
@@ -362,10 +364,10 @@ int ticket_slot(cudaStream_t stream) {
     return kEagerSlots + static_cast<int>(c);
 }
 
-template <int kFmt, int kN>
+template <int kFmt, int kN, bool kSplit = false>
 void launch_gemms_n(const std::vector<GemmSpec>& specs_in, cudaStream_t stream) {
     using T = GemmTraits<kFmt, kN>;
-    auto kernel = umma_gemm_kernel<kFmt, kN>;
+    auto kernel = umma_gemm_kernel<kFmt, kN, kSplit>;
     // Longest per-tile K first (problems of one launch are independent): the
     // block scheduler hands out CTAs roughly in blockIdx order, so long tiles
     // queued last would run as a tail on few SMs (the preconditioner mixes
@@ -409,12 +411,12 @@ void launch_gemms_n(const std::vector<GemmSpec>& specs_in, cudaStream_t stream) 
             if (gemm_persist_enabled() && kmin > 512 && tiles > sm_count()) {
                 static std::once_flag once;
                 std::call_once(once, [] {
-                    check(cudaFuncSetAttribute(umma_gemm_persist_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                    check(cudaFuncSetAttribute(umma_gemm_persist_kernel<kSplit>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                                T::kSmemBytes),
                           "cudaFuncSetAttribute(gemm persist)");
                 });
                 const int slot = ticket_slot(stream);
-                launch(umma_gemm_persist_kernel, dim3(std::min(tiles, sm_count())), dim3(kPersistThreads),
+                launch(umma_gemm_persist_kernel<kSplit>, dim3(std::min(tiles, sm_count())), dim3(kPersistThreads),
                        T::kSmemBytes, stream, batch, slot);
                 after_launch("umma_gemm_persist_kernel");
                 continue;
@@ -457,6 +459,12 @@ int pick_tile_n(const std::vector<GemmSpec>& specs) {
 
 void gemm_bf16(const std::vector<GemmSpec>& s, cudaStream_t st) { launch_gemms_n<kBF16, 128>(s, st); }
 void gemm_oz8(const std::vector<GemmSpec>& s, cudaStream_t st) {
+    if (!s.empty() && (s.front().flags & EPI_DIAG_SPLIT)) {  // the LAUUM (mirrored: 128-wide tiles)
+        for (const GemmSpec& g : s)
+            if (!(g.flags & EPI_DIAG_SPLIT)) throw std::logic_error("gemm_oz8: mixed EPI_DIAG_SPLIT launch");
+        launch_gemms_n<kOZ8, 128, true>(s, st);
+        return;
+    }
     switch (pick_tile_n(s)) {
         case 32: launch_gemms_n<kOZ8, 32>(s, st); break;
         case 64: launch_gemms_n<kOZ8, 64>(s, st); break;
@@ -786,15 +794,28 @@ struct StreamEmitter final : Emitter {
         ScopedPrio sp(prio);
         static std::once_flag once;
         std::call_once(once, [] {
-            check(cudaFuncSetAttribute(leaf_chol_inv_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+            check(cudaFuncSetAttribute(leaf_chol_inv_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       kLeafSmemBytes),
+                  "cudaFuncSetAttribute(leaf)");
+            check(cudaFuncSetAttribute(leaf_chol_inv_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                        kLeafSmemBytes),
                   "cudaFuncSetAttribute(leaf)");
         });
         for (std::size_t i = 0; i < ws.size(); i += kMaxLeafBatch) {
             LeafBatch b{};
             const int cnt = static_cast<int>(std::min<std::size_t>(kMaxLeafBatch, ws.size() - i));
-            for (int j = 0; j < cnt; ++j) b.e[j] = leaf_args(ws[i + j], o, n);
-            launch(leaf_chol_inv_kernel, dim3(cnt), dim3(kLeafThreads), kLeafSmemBytes, st, b);
+            bool with_l = false;
+            for (int j = 0; j < cnt; ++j) {
+                b.e[j] = leaf_args(ws[i + j], o, n);
+                with_l = with_l || b.e[j].l;
+            }
+            if (with_l) {
+                for (int j = 0; j < cnt; ++j)
+                    if (!b.e[j].l) throw std::invalid_argument("leaf batch mixes factor-only and inverse problems");
+                launch(leaf_chol_inv_kernel<true>, dim3(cnt), dim3(kLeafThreads), kLeafSmemBytes, st, b);
+            } else {
+                launch(leaf_chol_inv_kernel<false>, dim3(cnt), dim3(kLeafThreads), kLeafSmemBytes, st, b);
+            }
             after_launch("leaf_chol_inv_kernel");
         }
     }
@@ -1288,6 +1309,16 @@ bool use_recursive_inverse(const std::vector<const pf_inverse_problem*>& probs) 
     return w / dmax > kRecursiveFromW;
 }
 
+// PF_DIAG_SPLIT=0: the LAUUM slices X^T with its diagonal (measurement only:
+// the d = 4096 residual goes back from ~2e-6 to ~1e-5)
+bool diag_split_enabled() {
+    static const bool on = [] {
+        const char* e = std::getenv("PF_DIAG_SPLIT");
+        return !(e && e[0] == '0');
+    }();
+    return on;
+}
+
 void damped_inverse_group(const std::vector<const pf_inverse_problem*>& probs, Emitter& em, bool recursive) {
     const int d = probs.front()->d;
     std::vector<InvWs> ws;
@@ -1352,15 +1383,17 @@ void damped_inverse_group(const std::vector<const pf_inverse_problem*>& probs, E
     for (std::size_t i = 0; i < ws.size(); ++i) {
         const InvWs& w = ws[i];
         const pf_inverse_problem* p = probs[i];
-        sl.push_back(slice_of(w.xt, w.ld, 0, 0, d, d, w.s0, SLICE_UPPER_BLOCK | SLICE_ZERO_DIAG));
+        const bool split = diag_split_enabled();
+        sl.push_back(slice_of(w.xt, w.ld, 0, 0, d, d, w.s0, SLICE_UPPER_BLOCK | (split ? SLICE_ZERO_DIAG : 0)));
         GemmSpec s;
         s.a = sliced_view(w.s0, d, d);
         s.b = s.a;
         s.rows = s.cols = s.k = d;
         s.lower = true;
         s.k_mode = K_FROM_ROW_TILE;
-        s.flags = EPI_MIRROR | EPI_DIAG_SPLIT;
+        s.flags = EPI_MIRROR | (split ? EPI_DIAG_SPLIT : 0u);
         s.aux = w.x;  // X = L^-1, lower, ld = w.ld (multiple of 4, 256-B aligned plane)
+        s.aux_t = w.xt;
         s.ld_aux = w.ld;
         if (aligned16(p->minv) && p->ldinv % 4 == 0) s.flags |= EPI_VEC4;
         s.c = p->minv;

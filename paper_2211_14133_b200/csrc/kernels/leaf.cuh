@@ -439,6 +439,7 @@ __device__ __forceinline__ void store_l_panels(const float* PT, const LeafArgs& 
 
 // The whole leaf for one block, 256 threads, `leaf_smem` = kLeafSmemBytes of
 // 16-byte aligned shared memory.  `pdl`: called from a PDL-launched kernel.
+template <bool kWithL>
 __device__ __forceinline__ void leaf_body(const LeafArgs& A, float* leaf_smem, bool pdl) {
     float* Ls = leaf_smem;
     float* Xs = Ls + kLsFloats;
@@ -494,7 +495,7 @@ __device__ __forceinline__ void leaf_body(const LeafArgs& A, float* leaf_smem, b
         }
         __syncthreads();
         PF_STAMP(3 + 3 * p);
-        if (A.l) store_l_diag(LT, A, c0);  // LT stays untouched until the next phase A
+        if constexpr (kWithL) store_l_diag(LT, A, c0);  // LT stays untouched until the next phase A
         if (p == 3) break;
         // ---- B: TRSM of the rows below || X_pp
         const int below = kLeaf - c0 - 32;
@@ -536,16 +537,19 @@ __device__ __forceinline__ void leaf_body(const LeafArgs& A, float* leaf_smem, b
     for (int t = tid; t < 192; t += kLeafThreads) xprod_tile(XTd, Tb, Xs, 3, t / 24, t % 24);
     __syncthreads();
     PF_STAMP(14);
-    if (A.l) store_l_panels(PT, A);
+    if constexpr (kWithL) store_l_panels(PT, A);
     if (pdl) ptx::grid_dep_launch();
     store_x(Xs, Ls, A.x, A.xt, A.ld, A.n);
     PF_STAMP(19);
     if (tid == 0) report_bad(A.info, *bad);
 }
 
+// kWithL: the leaves of pf_cholesky_factor also write their block of L (a
+// separate instantiation, so the inverse's leaf keeps its register budget)
+template <bool kWithL>
 __global__ void __launch_bounds__(kLeafThreads, 1) leaf_chol_inv_kernel(const __grid_constant__ LeafBatch batch) {
     extern __shared__ __align__(16) float leaf_smem[];
-    leaf_body(batch.e[blockIdx.x], leaf_smem, true);
+    leaf_body<kWithL>(batch.e[blockIdx.x], leaf_smem, true);
 }
 
 }  // namespace pf

@@ -112,7 +112,8 @@ struct GemmDesc {
     float* c;
     float* c_t;
     int ldc, ldc_t;
-    const float* aux;  // EPI_DIAG_SPLIT: X (16-byte aligned rows, ld_aux % 4 == 0)
+    const float* aux;    // EPI_DIAG_SPLIT: X (16-byte aligned rows, ld_aux % 4 == 0)
+    const float* aux_t;  //   and X^T (same ld)
     int ld_aux;
 };
 
@@ -204,7 +205,7 @@ struct EpiRow {
     float dg = 0.0f;  // EPI_DIAG_SPLIT: X[r][r]
 };
 
-template <int kFmt, int kN = 128>
+template <int kFmt, int kN = 128, bool kSplit = false>
 __device__ __forceinline__ EpiRow epi_row(const GemmDesc& P, int tm, int tn, int r) {
     EpiRow e;
     (void)tm;
@@ -213,14 +214,16 @@ __device__ __forceinline__ EpiRow epi_row(const GemmDesc& P, int tm, int tn, int
             e.row_scale = P.alpha * ptx::pow2f(__ldcg(P.a_exp + r));
             if ((P.flags & EPI_EXACT_DIAG) && r >= tn * kN && r < (tn + 1) * kN)  // row's diagonal in this tile
                 e.diag_exact = static_cast<float>(__ldcg(P.a_sqnorm + r));  // = (norm 2^14) 2^-14
-            if (P.flags & EPI_DIAG_SPLIT) e.dg = __ldcg(P.aux + static_cast<size_t>(r) * P.ld_aux + r);
+            if (kSplit) e.dg = __ldcg(P.aux + static_cast<size_t>(r) * P.ld_aux + r);
         }
     }
     return e;
 }
 
 // col_scale: kOZ8 -> 2^e_b per tile column, kBF16 -> unused.
-template <int kFmt, int kN = 128>
+// kSplit: the EPI_DIAG_SPLIT variant (a separate instantiation: its extra
+// loads and registers stay out of every other digit GEMM)
+template <int kFmt, int kN = 128, bool kSplit = false>
 __device__ __forceinline__ void epilogue_chunks(const GemmDesc& P, int tm, int tn, uint32_t lane_base, int r,
                                                 const float* col_scale, int chunk_begin, int chunk_end,
                                                 bool have_acc, const EpiRow& er, const float* crow = nullptr) {
@@ -313,7 +316,8 @@ __device__ __forceinline__ void epilogue_chunks(const GemmDesc& P, int tm, int t
     };
     // EPI_DIAG_SPLIT: the diagonal's terms, exactly as one fp32 fma each
     auto split_fix = [&](float (&out)[16], int chunk) {
-        if (!(f & EPI_DIAG_SPLIT) || !row_ok) return;
+        if constexpr (!kSplit) return;
+        if (!row_ok) return;
         const int c0 = tn * kN + chunk * 16;
         const float* xr = P.aux + static_cast<size_t>(r) * P.ld_aux;
         if (c0 + 16 <= r) {  // left of the diagonal (every chunk of a lower off-diagonal tile)
@@ -328,19 +332,32 @@ __device__ __forceinline__ void epilogue_chunks(const GemmDesc& P, int tm, int t
             }
             return;
         }
-#pragma unroll 1
-        for (int j = 0; j < 16; ++j) {  // diagonal tiles
-            const int c = c0 + j;
-            if (c >= P.cols) break;
-            if (c < r) {
-                out[j] = fmaf(er.dg, __ldcg(xr + c), out[j]);
-            } else if (c > r) {
-                const float* xc = P.aux + static_cast<size_t>(c) * P.ld_aux;
-                out[j] = fmaf(__ldcg(xc + c), __ldcg(xc + r), out[j]);
-            } else {
-                out[j] = fmaf(er.dg, er.dg, out[j]);
+        // diagonal tiles: the row of X left of the diagonal, the row of X^T
+        // right of it (both contiguous), the diagonal X[c][c] (warp-uniform c);
+        // all loads issued before the fmas (fully unrolled: a runtime index
+        // into `out` would move it to local memory)
+        const float* tr = P.aux_t + static_cast<size_t>(r) * P.ld_aux;
+        float fa[16], fb[16];
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+            const int c = c0 + 4 * q;
+            // (rows are padded to ld_aux >= round_up(cols, 4): a float4 starting
+            // below cols stays inside the row; elements >= cols are dropped)
+            const bool any = c < P.cols;
+            const float4 lo = any && c < r ? __ldcg(reinterpret_cast<const float4*>(xr + c)) : make_float4(0.f, 0.f, 0.f, 0.f);
+            const float4 hi = any && c + 3 > r ? __ldcg(reinterpret_cast<const float4*>(tr + c)) : make_float4(0.f, 0.f, 0.f, 0.f);
+            const float l4[4] = {lo.x, lo.y, lo.z, lo.w}, h4[4] = {hi.x, hi.y, hi.z, hi.w};
+#pragma unroll
+            for (int e = 0; e < 4; ++e) {
+                const int cc = c + e;
+                const bool in = cc < P.cols;
+                const float dcc = in && cc > r ? __ldg(P.aux + static_cast<size_t>(cc) * P.ld_aux + cc) : 0.0f;
+                fa[4 * q + e] = !in ? 0.0f : cc < r ? er.dg : cc > r ? dcc : er.dg;
+                fb[4 * q + e] = !in ? 0.0f : cc < r ? l4[e] : cc > r ? h4[e] : er.dg;
             }
         }
+#pragma unroll
+        for (int j = 0; j < 16; ++j) out[j] = fmaf(fa[j], fb[j], out[j]);
     };
     if constexpr (kFmt == kOZ8) {
         if (!have_acc) {  // empty k-range
@@ -403,7 +420,7 @@ __device__ __forceinline__ void epilogue_chunks(const GemmDesc& P, int tm, int t
     }
 }
 
-template <int kFmt, int kN = 128>
+template <int kFmt, int kN = 128, bool kSplit = false>
 __global__ void __launch_bounds__(GemmTraits<kFmt, kN>::kThreads, GemmTraits<kFmt, kN>::kMinBlocks)
     umma_gemm_kernel(const __grid_constant__ GemmBatch batch) {
     using T = GemmTraits<kFmt, kN>;
@@ -560,7 +577,7 @@ __global__ void __launch_bounds__(GemmTraits<kFmt, kN>::kThreads, GemmTraits<kFm
     }
 
     // ---------------- epilogue: TMEM -> registers -> global
-    const EpiRow er = epi_row<kFmt, kN>(P, tm, tn, tm * kTile + (warp & 3) * 32 + static_cast<int>(lane));
+    const EpiRow er = epi_row<kFmt, kN, kSplit>(P, tm, tn, tm * kTile + (warp & 3) * 32 + static_cast<int>(lane));
     const bool have_acc = kb1 > kb0;
     if (have_acc) {
         ptx::mbar_wait(done, 0);
@@ -574,7 +591,7 @@ __global__ void __launch_bounds__(GemmTraits<kFmt, kN>::kThreads, GemmTraits<kFm
         constexpr int kPairs = T::kThreads / 128;  // warps sharing a TMEM lane quarter
         const int ew = warp & 3, part = warp >> 2;
         constexpr int kChunks = kN / 16 / kPairs;
-        epilogue_chunks<kFmt, kN>(P, tm, tn, tmem + (static_cast<uint32_t>(ew * 32) << 16),
+        epilogue_chunks<kFmt, kN, kSplit>(P, tm, tn, tmem + (static_cast<uint32_t>(ew * 32) << 16),
                               tm * kTile + ew * 32 + static_cast<int>(lane), col_scale, part * kChunks,
                               (part + 1) * kChunks, have_acc, er,
                               cpre ? cbuf + (ew * 32 + static_cast<int>(lane)) * T::kCStride : nullptr);
@@ -637,6 +654,7 @@ __device__ __forceinline__ void tile_of(const GemmBatch& batch, int gt, int& p, 
     kb1 = max(kb0, (k_end + kKB - 1) / kKB);
 }
 
+template <bool kSplit = false>
 __global__ void __launch_bounds__(kPersistThreads, 1)
     umma_gemm_persist_kernel(const __grid_constant__ GemmBatch batch, int slot) {
     using T = GemmTraits<kOZ8>;
@@ -786,13 +804,13 @@ __global__ void __launch_bounds__(kPersistThreads, 1)
                 col_scale[et] = c < P.cols ? ptx::pow2f(__ldcg(P.b_exp + c)) : 0.0f;
             }
             const int r = tm * kTile + ew * 32 + static_cast<int>(lane);
-            const EpiRow er = epi_row<kOZ8>(P, tm, tn, r);
+            const EpiRow er = epi_row<kOZ8, kTile, kSplit>(P, tm, tn, r);
             asm volatile("bar.sync 1, 256;" ::: "memory");
             ptx::mbar_wait(done, it & 1);
             ptx::tc_fence_after();
             __syncwarp();
             constexpr int kChunks = kTile / 16 / 2;
-            epilogue_chunks<kOZ8>(P, tm, tn, tmem + (static_cast<uint32_t>(ew * 32) << 16), r, col_scale,
+            epilogue_chunks<kOZ8, kTile, kSplit>(P, tm, tn, tmem + (static_cast<uint32_t>(ew * 32) << 16), r, col_scale,
                                   part * kChunks, (part + 1) * kChunks, kb1 > kb0, er);
             ptx::tc_fence_before();
             __syncwarp();
