@@ -24,14 +24,14 @@ int main() {
     cudaMalloc(&info, 4); cudaMalloc(&stamps, 64 * 8); cudaMemset(stamps, 0, 64 * 8);
     cudaMemcpy(da, a.data(), n * n * 4, cudaMemcpyHostToDevice);
     cudaMemset(info, 0, 4);
-    cudaFuncSetAttribute(leaf_chol_inv_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kLeafSmemBytes);
+    cudaFuncSetAttribute(leaf_chol_inv_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, kLeafSmemBytes);
     LeafBatch b{};
     b.e[0] = LeafArgs{da, dx, dxt, info, ld, n, 0};
     cudaMemcpyToSymbol(g_probe, &stamps, sizeof(stamps));
     cudaEvent_t e0, e1; cudaEventCreate(&e0); cudaEventCreate(&e1);
-    for (int it = 0; it < 5; ++it) leaf_chol_inv_kernel<<<1, kLeafThreads, kLeafSmemBytes>>>(b);
+    for (int it = 0; it < 5; ++it) leaf_chol_inv_kernel<false><<<1, kLeafThreads, kLeafSmemBytes>>>(b);
     cudaEventRecord(e0);
-    for (int it = 0; it < 20; ++it) leaf_chol_inv_kernel<<<1, kLeafThreads, kLeafSmemBytes>>>(b);
+    for (int it = 0; it < 20; ++it) leaf_chol_inv_kernel<false><<<1, kLeafThreads, kLeafSmemBytes>>>(b);
     cudaEventRecord(e1);
     cudaDeviceSynchronize();
     float ms; cudaEventElapsedTime(&ms, e0, e1);
