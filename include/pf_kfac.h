@@ -141,6 +141,14 @@ int pf_f32_to_bf16(const float* x, int64_t n, void* out_bf16, void* stream);
 /* Number of kernels this library launched since load (evidence counter for
  * bench.py's gpu_launches; incremented per launch on the host). */
 int64_t pf_kernel_launch_count(void);
+/* Background mode for the calling host thread (1 = on, 0 = off; returns the
+ * previous setting).  On: every launch of later calls goes at the device's
+ * least priority and long-K GEMMs run one CTA per tile (no persistent CTAs),
+ * so the calls can run on a second stream UNDER a latency-bound inversion
+ * chain without holding the SMs that chain needs.  Results are unchanged
+ * (bit-identical): scheduling only.  No reference counterpart (the reference
+ * is single-threaded CPU code). */
+int pf_set_background(int on);
 /* 1 if a device with compute capability 10.x is visible. */
 int pf_device_ok(void);
 

@@ -123,6 +123,7 @@ _SIGNATURES = {
     "pf_f32_to_bf16": (C.c_int, [C.c_void_p, C.c_int64, C.c_void_p, C.c_void_p]),
     "pf_kernel_launch_count": (C.c_int64, []),
     "pf_device_ok": (C.c_int, []),
+    "pf_set_background": (C.c_int, [C.c_int]),
 }
 
 _lock = threading.Lock()

@@ -334,12 +334,20 @@ inline int desc_tiles(const GemmDesc& d) { return d.lower ? d.tiles_m * (d.tiles
 
 int sm_count();
 
+// Background calls (pf_set_background, per host thread): work issued to run
+// UNDER a latency-bound chain on another stream (e.g. a layer's 1024-wide
+// factors while its 4096-wide chains run).  Every launch of the call goes at
+// the device's least priority and long-K GEMMs use one CTA per tile instead
+// of persistent CTAs, so a critical kernel of the other stream gets the next
+// free SM within one tile instead of after the whole persistent launch.
+thread_local bool g_background = false;
+
 bool gemm_persist_enabled() {  // PF_GEMM_PERSIST=0: one CTA per tile for long-K launches too (A/B)
     static const bool on = [] {
         const char* e = std::getenv("PF_GEMM_PERSIST");
         return !(e && e[0] == '0');
     }();
-    return on;
+    return on && !g_background;
 }
 
 // Ticket counter of one persistent-GEMM launch (g_tickets, umma_gemm.cuh).
@@ -741,7 +749,7 @@ struct StreamEmitter final : Emitter {
     // (2x4096 + 10x1024: 3.07 -> 2.97 ms).
     explicit StreamEmitter(cudaStream_t s, int g = 0, bool lead = true) : st(s), main(s), group(g) {
         const auto [least, greatest] = prio_range();
-        prio_main = prio = lead ? greatest : least;
+        prio_main = prio = lead && !g_background ? greatest : least;
         prio_side = least;
     }
     void side_begin(int depth) override {
@@ -1569,6 +1577,23 @@ int pf_gemm_probe_read(long long* out) {  // 64 records of 8; returns the record
     return n;
 }
 #endif
+
+#ifdef PF_LEAF_RING
+int pf_leaf_ring_read(long long* out) {  // 64 records of 8; returns the record count, resets it
+    int n = 0;
+    if (cudaMemcpyFromSymbol(out, pf::g_leaf_ring, sizeof(long long) * 64 * 8) != cudaSuccess) return -1;
+    if (cudaMemcpyFromSymbol(&n, pf::g_leaf_ring_n, sizeof(int)) != cudaSuccess) return -1;
+    const int zero = 0;
+    cudaMemcpyToSymbol(pf::g_leaf_ring_n, &zero, sizeof(int));
+    return n;
+}
+#endif
+
+int pf_set_background(int on) {
+    const int was = pf::g_background ? 1 : 0;
+    pf::g_background = on != 0;
+    return was;
+}
 
 int pf_device_ok(void) {
     int dev = 0;

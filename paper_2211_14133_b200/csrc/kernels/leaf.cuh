@@ -23,13 +23,14 @@
 //   C  trailing update of the NEXT panel's block column only (all that the
 //      next Cholesky needs) and X[p, 0:p] = -X_pp T_p.
 // All products are 4x4 register tiles fed by float4 shared-memory reads of
-// k-major copies (PT_p = panel transposed, LT / XTd = diagonal blocks
+// k-major copies (PT_p = panel transposed, LB / XTd = diagonal blocks
 // transposed), skipping the structurally-zero triangles.
 #pragma once
 
 #include <cfloat>
 #include <climits>
 #include <cstdint>
+#include <utility>
 
 #include "ptx.cuh"
 
@@ -56,6 +57,19 @@ __device__ long long* g_probe;
     } while (0)
 #endif
 
+#ifdef PF_LEAF_RING
+// in-situ probe (-DPF_LEAF_RING): CTA 0 of every leaf launch records
+// {globaltimer at entry, after griddepcontrol.wait, after the load, at the
+// end; clock64 at entry and end} into a 64-entry ring
+__device__ long long g_leaf_ring[64 * 8];
+__device__ int g_leaf_ring_n;
+__device__ __forceinline__ long long leaf_gtimer() {
+    long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    return t;
+}
+#endif
+
 constexpr int kLeaf = 128;
 constexpr int kLeafThreads = 256;
 constexpr int kLeafWarps = kLeafThreads / 32;
@@ -63,7 +77,7 @@ constexpr int kMaxLeafBatch = 32;
 // shared-memory layout (floats; every array 16-byte aligned)
 constexpr int kLeafPitch = 129;   // Ls: active trailing matrix (column walks conflict-free)
 constexpr int kXPitch = 132;      // Xs, PT: float4 rows
-constexpr int kSmallPitch = 36;   // LT, XTd: transposed 32x32 diagonal blocks
+constexpr int kSmallPitch = 36;   // LB (shifted columns of L_pp), XTd (X_pp transposed)
 // Tb: T_1, T_2, T_3 (32 x 32bi, pitch 32bi + 4), accumulated panel by panel
 __host__ __device__ constexpr int t_pitch(int bi) { return 32 * bi + 4; }
 __host__ __device__ constexpr int t_offset(int bi) { return bi == 1 ? 0 : bi == 2 ? 32 * t_pitch(1) : 32 * (t_pitch(1) + t_pitch(2)); }
@@ -126,16 +140,101 @@ __device__ __forceinline__ void lower_pair(int t, int& i, int& j) {
 }
 
 // ---- phase A, warp 0: Cholesky of the 32x32 diagonal block at (c0, c0) of Ls.
-// Writes LT[j][i] = L[i][j] (zeros above the diagonal) and rdiag = 1/L[k][k].
-// Lane i owns row i; entries above the diagonal pick up garbage in registers
-// but never feed a value that is kept.
+// Lane i owns row i.  The three 32-step loops of the leaf (chol32, trsm_row,
+// inv32) are ROLLED: the leaf's code must stay inside the SM's 32 KB L1.5
+// instruction cache (fully unrolled the leaf was 126 KB of SASS and ran 30 %
+// slower in cycles whenever a concurrent GEMM loaded L2, instruction fetch
+// from L2 being on its critical path).  Rolling keeps every register index
+// static by ROTATING the row: at pivot k, a[0] holds column k and the update
+// of column k + m writes a[m - 1], so the array shifts by one per step at no
+// extra cost (the FMA's destination is the shifted slot).  The arithmetic is
+// the reference order, operation for operation: a[j] -= l_i l_j per pivot,
+// pivots by rsqrt (the unrolled form produced the same bits).
+//
+// Writes LB[k][m] = L[k + 1 + m][k] (column k below the diagonal, shifted to
+// start at m = 0, zero-padded to 32: aligned float4 rows for the TRSM and the
+// inverse), rdiag[c0 + k] = 1 / L[k][k] and, kWithL, ldiag[k] = L[k][k].
 __device__ __forceinline__ float rsqrt_ftz(float x) {
     float y;
     asm("rsqrt.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
     return y;
 }
 
-__device__ __forceinline__ void chol32(const float* Ls, float* LT, float* rdiag, float* lbuf, int c0, int n,
+// Steps per rolled loop of chol32 / trsm_row / inv32 (the width shrinks by
+// kPhase from one loop to the next).
+#ifndef PF_LEAF_PHASE
+#define PF_LEAF_PHASE 8
+#endif
+constexpr int kPhase = PF_LEAF_PHASE;
+#ifndef PF_LEAF_UNROLL
+#define PF_LEAF_UNROLL 2
+#endif
+constexpr int kLeafUnroll = PF_LEAF_UNROLL;
+
+// First W floats of an LB row (aligned float4 loads).
+template <int W>
+__device__ __forceinline__ void lb_load(const float* lb, float4 (&v)[W / 4]) {
+#pragma unroll
+    for (int q = 0; q < W / 4; ++q) v[q] = *reinterpret_cast<const float4*>(lb + 4 * q);
+}
+
+// One rotated elimination step on an array of width W:
+// a[m] = a[m + 1] + s * lv[m] for m < W - 1 (lv = the first W floats of an LB row).
+template <int W>
+__device__ __forceinline__ void rot_step(float (&a)[32], float s, const float4 (&v)[W / 4]) {
+#pragma unroll
+    for (int q = 0; q < W / 4; ++q) {
+        const float lv[4] = {v[q].x, v[q].y, v[q].z, v[q].w};
+#pragma unroll
+        for (int e = 0; e < 4; ++e)
+            if (4 * q + e < W - 1) a[4 * q + e] = fmaf(s, lv[e], a[4 * q + e + 1]);
+    }
+}
+
+// The 32 steps of each loop run as 32 / kPhase rolled loops of kPhase steps
+// over a shrinking width (32, 28, ..., 4): after step k only 32 - k - 1
+// entries are live, so each loop touches at most kPhase - 1 dead ones (544
+// FMAs per row for kPhase = 4, against 496 unrolled or 992 fully rolled) and
+// the code stays a few short loop bodies.
+//
+// chol32: the pivot chain is software-pipelined across iterations -- the
+// next pivot (shuffle of the updated diagonal + rsqrt) is issued as soon as
+// this pivot's l is known, and the next column's value reaches a[0] through
+// one shuffle instead of the shared-memory round trip the rest of the row
+// update takes.  Same operations in the same order as the plain loop.
+template <bool kWithL, int W>
+__device__ __forceinline__ void chol32_steps(float (&a)[32], float& dii, float& piv, float& rl, float& mypiv,
+                                             int k0, float* LB, float* rdiag, float* ldiag, int c0) {
+    const int lane = threadIdx.x & 31;
+#pragma unroll(kLeafUnroll)
+    for (int k = k0; k < k0 + kPhase; ++k) {
+        const float l = lane > k ? a[0] * rl : (lane == k ? piv * rl : 0.0f);
+        dii = fmaf(-l, l, dii);
+        // lanes > k publish their l at lane - k - 1; lanes <= k zero the tail
+        // of the row (index 31 - k + lane: the same expression mod 32)
+        LB[k * kSmallPitch + ((lane - k - 1) & 31)] = lane > k ? l : 0.0f;
+        // the next pivot: lane k + 1's diagonal is final once its l is known
+        const float piv_n = __shfl_sync(0xffffffffu, dii, (k + 1) & 31);
+        const float l_k1 = __shfl_sync(0xffffffffu, l, (k + 1) & 31);  // L[k + 1][k] = LB[k][0]
+        if (lane == k) {
+            mypiv = piv;  // checked after the loop
+            rdiag[c0 + k] = rl;
+            if (kWithL) ldiag[k] = l;
+        }
+        const float rl_n = rsqrt_ftz(piv_n);
+        const float a0 = fmaf(-l, l_k1, a[1]);
+        __syncwarp();
+        float4 v[W / 4];
+        lb_load<W>(LB + k * kSmallPitch, v);
+        rot_step<W>(a, -l, v);
+        a[0] = a0;
+        piv = piv_n;
+        rl = rl_n;
+    }
+}
+
+template <bool kWithL>
+__device__ __forceinline__ void chol32(const float* Ls, float* LB, float* rdiag, float* ldiag, int c0, int n,
                                        int col_base, int* bad) {
     const int lane = threadIdx.x & 31;
     const float* row = Ls + (c0 + lane) * kLeafPitch + c0;
@@ -143,98 +242,89 @@ __device__ __forceinline__ void chol32(const float* Ls, float* LT, float* rdiag,
 #pragma unroll
     for (int j = 0; j < 32; ++j) a[j] = row[j];
     float dii = row[lane];  // == a[lane], kept apart so the pivot chain is short
-    int badcol = INT_MAX;
-#pragma unroll
-    for (int k = 0; k < 32; ++k) {
-        const float piv = __shfl_sync(0xffffffffu, dii, k);  // warp-uniform
-#ifdef PF_CHOL_OLDPIV
-        const bool ok = piv > 0.0f && piv <= FLT_MAX;
-        const float pv = ok ? piv : 1.0f;
-        const float rl = rsqrtf(pv);
-#else
-        // a failed pivot (<= 0, inf, NaN) is recorded and then propagates NaN /
-        // inf through the block; the caller raises on info != 0
-        const bool ok = piv > 0.0f && piv <= FLT_MAX;
-        const float pv = piv;
-        const float rl = rsqrt_ftz(piv);
-#endif
-        if (!ok && c0 + k < n && badcol == INT_MAX) badcol = col_base + c0 + k + 1;
-        const float l = lane > k ? a[k] * rl : (lane == k ? pv * rl : 0.0f);
-        a[k] = l;
-        dii = fmaf(-l, l, dii);
-        if (lane == k) rdiag[c0 + k] = rl;
-#ifdef PF_CHOL_SHFL
-#pragma unroll
-        for (int j = k + 1; j < 32; ++j) a[j] = fmaf(-l, __shfl_sync(0xffffffffu, l, j), a[j]);
-#else
-        // broadcast l through shared memory (double-buffered by step parity)
-        float* lb = lbuf + 32 * (k & 1);
-        lb[lane] = l;
-        __syncwarp();
-#pragma unroll
-        for (int q4 = (k + 1) / 4; q4 < 8; ++q4) {
-            const float4 v = *reinterpret_cast<const float4*>(lb + 4 * q4);
-            const float lv[4] = {v.x, v.y, v.z, v.w};
-#pragma unroll
-            for (int e = 0; e < 4; ++e)
-                if (4 * q4 + e > k) a[4 * q4 + e] = fmaf(-l, lv[e], a[4 * q4 + e]);
-        }
-#endif
-    }
-    if (lane == 0 && badcol != INT_MAX) *bad = min(*bad, badcol);
-#pragma unroll
-    for (int j = 0; j < 32; ++j) LT[j * kSmallPitch + lane] = j <= lane ? a[j] : 0.0f;
+    float piv = __shfl_sync(0xffffffffu, dii, 0);  // warp-uniform
+    float rl = rsqrt_ftz(piv);
+    float mypiv = 1.0f;
+    [&]<int... P>(std::integer_sequence<int, P...>) {
+        (chol32_steps<kWithL, 32 - kPhase * P>(a, dii, piv, rl, mypiv, kPhase * P, LB, rdiag, ldiag, c0), ...);
+    }(std::make_integer_sequence<int, 32 / kPhase>{});
+    // a failed pivot (<= 0, inf, NaN) propagated NaN / inf through the block;
+    // the first one (1-based column) goes to *bad, the caller raises on it
+    const unsigned failed = __ballot_sync(0xffffffffu, !(mypiv > 0.0f && mypiv <= FLT_MAX) && c0 + lane < n);
+    if (lane == 0 && failed) *bad = min(*bad, col_base + c0 + __ffs(failed));
 }
 
 // ---- phase B: row r of the panel solve  L[r, p] = A[r, p] L_pp^-T  by
 // forward substitution (x_j final -> eliminate it from the later entries;
-// reference matrix.cpp order), result stored transposed: PTp[k][r].
-__device__ __forceinline__ void trsm_row(const float* Ls, const float* LT, const float* rdiag, float* PTp,
+// reference matrix.cpp order), result stored transposed: PTp[k][r].  Rotated
+// like chol32; the next step's LB row and 1/L_jj are loaded one step ahead.
+template <int W>
+__device__ __forceinline__ void trsm_steps(float (&x)[32], int j0, const float* LB, const float* rdiag,
+                                           float* PTp, int c0, int r) {
+    float4 nv[W / 4];
+    lb_load<W>(LB + j0 * kSmallPitch, nv);
+    float rd_n = rdiag[c0 + j0];
+#pragma unroll(kLeafUnroll)
+    for (int j = j0; j < j0 + kPhase; ++j) {
+        float4 v[W / 4];
+#pragma unroll
+        for (int q = 0; q < W / 4; ++q) v[q] = nv[q];
+        const float rd = rd_n;
+        if (j + 1 < j0 + kPhase) {
+            lb_load<W>(LB + (j + 1) * kSmallPitch, nv);
+            rd_n = rdiag[c0 + j + 1];
+        }
+        const float xj = x[0] * rd;
+        PTp[j * kXPitch + r] = xj;
+        rot_step<W>(x, -xj, v);
+    }
+}
+
+__device__ __forceinline__ void trsm_row(const float* Ls, const float* LB, const float* rdiag, float* PTp,
                                          int c0, int r) {
     const float* row = Ls + r * kLeafPitch + c0;
     float x[32];
 #pragma unroll
     for (int j = 0; j < 32; ++j) x[j] = row[j];
-#pragma unroll
-    for (int j = 0; j < 32; ++j) {
-        x[j] *= rdiag[c0 + j];
-#pragma unroll
-        for (int q4 = (j + 1) / 4; q4 < 8; ++q4) {
-            const float4 v = *reinterpret_cast<const float4*>(LT + j * kSmallPitch + 4 * q4);
-            const float lv[4] = {v.x, v.y, v.z, v.w};
-#pragma unroll
-            for (int e = 0; e < 4; ++e)
-                if (4 * q4 + e > j) x[4 * q4 + e] = fmaf(-x[j], lv[e], x[4 * q4 + e]);
-        }
-    }
-#pragma unroll
-    for (int k = 0; k < 32; ++k) PTp[k * kXPitch + r] = x[k];
+    [&]<int... P>(std::integer_sequence<int, P...>) {
+        (trsm_steps<32 - kPhase * P>(x, kPhase * P, LB, rdiag, PTp, c0, r), ...);
+    }(std::make_integer_sequence<int, 32 / kPhase>{});
 }
 
 // ---- phase B, one warp: X_pp = L_pp^-1 (lane c computes column c, reference
 // matrix.cpp:145-153); into Xs (zeros above the diagonal) and XTd[c][i] = X[i][c].
-__device__ __forceinline__ void inv32(const float* LT, const float* rdiag, float* Xs, float* XTd, int c0) {
+template <int W>
+__device__ __forceinline__ void inv32_steps(float (&x)[32], int i0, const float* LB, const float* rdiag,
+                                            float* Xs, float* XTd, int c0) {
+    const int lane = threadIdx.x & 31;
+    float4 nv[W / 4];
+    lb_load<W>(LB + i0 * kSmallPitch, nv);
+    float rd_n = rdiag[c0 + i0];
+#pragma unroll(kLeafUnroll)
+    for (int i = i0; i < i0 + kPhase; ++i) {
+        float4 v[W / 4];
+#pragma unroll
+        for (int q = 0; q < W / 4; ++q) v[q] = nv[q];
+        const float rd = rd_n;
+        if (i + 1 < i0 + kPhase) {
+            lb_load<W>(LB + (i + 1) * kSmallPitch, nv);
+            rd_n = rdiag[c0 + i + 1];
+        }
+        const float xi = x[0] * rd;
+        Xs[(c0 + i) * kXPitch + c0 + lane] = xi;
+        XTd[lane * kSmallPitch + i] = xi;
+        rot_step<W>(x, -xi, v);  // fmaf(-xi, L, x) == fmaf(-L, xi, x) exactly
+    }
+}
+
+__device__ __forceinline__ void inv32(const float* LB, const float* rdiag, float* Xs, float* XTd, int c0) {
     const int lane = threadIdx.x & 31;
     float x[32];
 #pragma unroll
     for (int i = 0; i < 32; ++i) x[i] = (i == lane) ? 1.0f : 0.0f;
-#pragma unroll
-    for (int i = 0; i < 32; ++i) {
-        x[i] *= rdiag[c0 + i];
-#pragma unroll
-        for (int q4 = (i + 1) / 4; q4 < 8; ++q4) {
-            const float4 v = *reinterpret_cast<const float4*>(LT + i * kSmallPitch + 4 * q4);
-            const float lv[4] = {v.x, v.y, v.z, v.w};
-#pragma unroll
-            for (int e = 0; e < 4; ++e)
-                if (4 * q4 + e > i) x[4 * q4 + e] = fmaf(-lv[e], x[i], x[4 * q4 + e]);
-        }
-    }
-#pragma unroll
-    for (int i = 0; i < 32; ++i) Xs[(c0 + i) * kXPitch + c0 + lane] = x[i];
-#pragma unroll
-    for (int i = 0; i < 32; i += 4)
-        *reinterpret_cast<float4*>(XTd + lane * kSmallPitch + i) = make_float4(x[i], x[i + 1], x[i + 2], x[i + 3]);
+    [&]<int... P>(std::integer_sequence<int, P...>) {
+        (inv32_steps<32 - kPhase * P>(x, kPhase * P, LB, rdiag, Xs, XTd, c0), ...);
+    }(std::make_integer_sequence<int, 32 / kPhase>{});
 }
 
 // trailing-update tile: Ls[r][c] -= sum_k L[r][k] L[c][k] over panel PTp, for
@@ -420,11 +510,13 @@ __device__ __forceinline__ void report_bad(int* info, int bad) {
     }
 }
 
-// pf_cholesky_factor: the 32x32 diagonal block c0 of L from LT (LT[j][i] = L[i][j])
-__device__ __forceinline__ void store_l_diag(const float* LT, const LeafArgs& A, int c0) {
+// pf_cholesky_factor: the 32x32 diagonal block c0 of L from LB / ldiag
+// (L[i][j] = LB[j][i - j - 1] below the diagonal, ldiag[j] on it)
+__device__ __forceinline__ void store_l_diag(const float* LB, const float* ldiag, const LeafArgs& A, int c0) {
     for (int idx = threadIdx.x; idx < 32 * 32; idx += kLeafThreads) {
         const int i = idx >> 5, j = idx & 31;
-        if (j <= i && c0 + i < A.n) A.l[static_cast<size_t>(c0 + i) * A.ldl + c0 + j] = LT[j * kSmallPitch + i];
+        if (j <= i && c0 + i < A.n)
+            A.l[static_cast<size_t>(c0 + i) * A.ldl + c0 + j] = i == j ? ldiag[j] : LB[j * kSmallPitch + i - j - 1];
     }
 }
 // ... and the panels below the diagonal blocks, PT_p[k][r] = L[r][32p + k]
@@ -437,6 +529,25 @@ __device__ __forceinline__ void store_l_panels(const float* PT, const LeafArgs& 
         }
 }
 
+// Helper warps of a phase: warps in [first, last] whose scheduler (warp % 4)
+// is not in `sched_mask`, so the critical warps keep their issue slots.
+// Returns the warp's rank among them and their count.
+__device__ __forceinline__ bool helper_warp(int warp, unsigned sched_mask) {
+    return !((sched_mask >> (warp & 3)) & 1u);
+}
+__device__ __forceinline__ int helper_rank(int warp, unsigned sched_mask, int& count, int first, int last) {
+    int rank = 0;
+    count = 0;
+#pragma unroll
+    for (int w = 0; w < kLeafWarps; ++w) {
+        if (w > last) break;
+        const bool ok = w >= first && helper_warp(w, sched_mask);
+        if (ok && w < warp) ++rank;
+        count += ok ? 1 : 0;
+    }
+    return rank;
+}
+
 // The whole leaf for one block, 256 threads, `leaf_smem` = kLeafSmemBytes of
 // 16-byte aligned shared memory.  `pdl`: called from a PDL-launched kernel.
 template <bool kWithL>
@@ -444,18 +555,24 @@ __device__ __forceinline__ void leaf_body(const LeafArgs& A, float* leaf_smem, b
     float* Ls = leaf_smem;
     float* Xs = Ls + kLsFloats;
     float* PT = Xs + kXsFloats;  // panels 0..2, transposed
-    float* LT = PT + 3 * kPTFloats;
-    float* XTd = LT + kSmallFloats;
+    float* LB = PT + 3 * kPTFloats;  // chol32's shifted columns of L_pp
+    float* XTd = LB + kSmallFloats;
     float* Tb = XTd + kSmallFloats;
-    float* lbuf = Tb + kTbFloats;  // chol32 broadcast buffer, 2 x 32
-    float* rdiag = lbuf + 64;
+    float* ldiag = Tb + kTbFloats;  // kWithL: the diagonal of L_pp (64 floats reserved)
+    float* rdiag = ldiag + 64;
     int* bad = reinterpret_cast<int*>(rdiag + kLeaf);
     const int tid = threadIdx.x;
     const int warp = tid >> 5;
 
     PF_STAMP(0);
+#ifdef PF_LEAF_RING
+    long long r_t0 = leaf_gtimer(), r_c0 = clock64(), r_t1 = 0, r_t2 = 0;
+#endif
     if (tid == 0) *bad = INT_MAX;
     if (pdl) ptx::grid_dep_wait();  // PDL: A is produced by the previous launch
+#ifdef PF_LEAF_RING
+    r_t1 = leaf_gtimer();
+#endif
     const bool vec = A.n == kLeaf && (A.ld % 4 == 0) && ((reinterpret_cast<uintptr_t>(A.a) & 15) == 0);
     if (vec) {
         float4 v[kLoadPer];
@@ -468,20 +585,27 @@ __device__ __forceinline__ void leaf_body(const LeafArgs& A, float* leaf_smem, b
     }
     __syncthreads();
     PF_STAMP(2);
+#ifdef PF_LEAF_RING
+    r_t2 = leaf_gtimer();
+#endif
 
+#pragma unroll 1
     for (int p = 0; p < 4; ++p) {
         const int c0 = 32 * p;
         // ---- A: chol(p) || rest of U(p-1) + T_p
         if (warp == 0) {
-            chol32(Ls, LT, rdiag, lbuf, c0, A.n, A.col0, bad);
+            chol32<kWithL>(Ls, LB, rdiag, ldiag, c0, A.n, A.col0, bad);
             PF_STAMP_T(20 + p, 0);
-        } else if (p > 0) {
+        } else if (p > 0 && helper_warp(warp, 1u)) {
             // rest of U(p-1) + panel p-1's contribution to T_p (the later T_bi
-            // get theirs on the idle warps of phase B)
+            // get theirs on the idle warps of phase B), on the warps that do
+            // not share warp 0's scheduler (warp w issues on scheduler w % 4)
             const int base = 8 * (p + 1), m = 32 - base;  // tile rows/cols [base, 32), lower
             const int nrest = m * (m + 1) / 2;
             const int per = 64 * p;                       // tiles of one T_bi slice (8 x 8p)
-            for (int t = tid - 32; t < nrest + per; t += kLeafThreads - 32) {
+            int nh;
+            const int h = helper_rank(warp, 1u, nh, 1, kLeafWarps - 1);
+            for (int t = h * 32 + (tid & 31); t < nrest + per; t += nh * 32) {
                 if (t < nrest) {
                     int i, j;
                     lower_pair(t, i, j);
@@ -495,15 +619,17 @@ __device__ __forceinline__ void leaf_body(const LeafArgs& A, float* leaf_smem, b
         }
         __syncthreads();
         PF_STAMP(3 + 3 * p);
-        if constexpr (kWithL) store_l_diag(LT, A, c0);  // LT stays untouched until the next phase A
+        if constexpr (kWithL) store_l_diag(LB, ldiag, A, c0);  // LB stays untouched until the next phase A
         if (p == 3) break;
         // ---- B: TRSM of the rows below || X_pp
         const int below = kLeaf - c0 - 32;
         if (tid < below) {
-            trsm_row(Ls, LT, rdiag, PT + p * kPTFloats, c0, c0 + 32 + tid);
+            trsm_row(Ls, LB, rdiag, PT + p * kPTFloats, c0, c0 + 32 + tid);
         } else if (warp == kLeafWarps - 1) {
-            inv32(LT, rdiag, Xs, XTd, c0);
+            inv32(LB, rdiag, Xs, XTd, c0);
         } else if (p > 0) {  // warps between: panel p-1's contribution to T_{p+1} .. T_3
+            // (keeping them off the schedulers of the TRSM / X_pp warps was
+            // measured slower: too few warps left for this work at p = 1)
             const int first = (below + 31) / 32 * 32;  // first thread of the free warps
             const int per = 64 * p, n = per * (3 - p);
             for (int t = tid - first; t >= 0 && t < n; t += (kLeafWarps - 1) * 32 - first) {
@@ -531,16 +657,28 @@ __device__ __forceinline__ void leaf_body(const LeafArgs& A, float* leaf_smem, b
         PF_STAMP(5 + 3 * p);
     }
     // ---- tail: X_33, then X[3, 0:3] = -X_33 T_3
-    if (warp == 0) inv32(LT, rdiag, Xs, XTd, 96);
+    if (warp == 0) inv32(LB, rdiag, Xs, XTd, 96);
     __syncthreads();
     PF_STAMP(13);
     for (int t = tid; t < 192; t += kLeafThreads) xprod_tile(XTd, Tb, Xs, 3, t / 24, t % 24);
     __syncthreads();
     PF_STAMP(14);
     if constexpr (kWithL) store_l_panels(PT, A);
+#ifdef PF_LEAF_RING
+    const long long r_t3 = leaf_gtimer();
+#endif
     if (pdl) ptx::grid_dep_launch();
     store_x(Xs, Ls, A.x, A.xt, A.ld, A.n);
     PF_STAMP(19);
+#ifdef PF_LEAF_RING
+    __syncthreads();
+    if (tid == 0 && blockIdx.x == 0) {
+        const int i = atomicAdd(&g_leaf_ring_n, 1) & 63;
+        long long* rec = g_leaf_ring + 8 * i;
+        rec[0] = r_t0; rec[1] = r_t1; rec[2] = r_t2; rec[3] = leaf_gtimer();
+        rec[4] = r_c0; rec[5] = clock64(); rec[6] = r_t3; rec[7] = A.col0;
+    }
+#endif
     if (tid == 0) report_bad(A.info, *bad);
 }
 

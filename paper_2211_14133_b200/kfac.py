@@ -55,6 +55,21 @@ def kernel_launches() -> int:
     return int(L.lib().pf_kernel_launch_count())
 
 
+class background:
+    """Context manager: calls issued inside run in background mode on this
+    host thread (pf_set_background): least launch priority, no persistent
+    GEMM CTAs -- for work placed on a second stream under a latency-bound
+    inversion chain.  Results are bit-identical to a normal call."""
+
+    def __enter__(self):
+        self._was = L.lib().pf_set_background(1)
+        return self
+
+    def __exit__(self, *exc):
+        L.lib().pf_set_background(self._was)
+        return False
+
+
 class _Workspaces:
     """Scratch arena per (device, tag, stream): grows, never shrinks; hot calls
     allocate nothing.  Keyed by the launching stream because calls on

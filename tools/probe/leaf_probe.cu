@@ -4,10 +4,30 @@
 #include <cstdlib>
 #include <vector>
 #include <cmath>
+#include <string>
 #include "leaf.cuh"
 using namespace pf;
 
-int main() {
+// Contention modes (argv[1]): "mem" = 147 CTAs stream a 1 GiB buffer
+// (read + write, ~BR's HBM traffic pattern) on a second stream while the
+// leaf runs; "spin" = 147 CTAs of FFMA chains (SM load, no memory traffic);
+// "l2" = 147 CTAs re-reading a 32 MiB buffer (L2-resident traffic).
+__global__ void busy_mem(float4* buf, size_t n4, int reps) {
+    for (int r = 0; r < reps; ++r)
+        for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < n4; i += (size_t)gridDim.x * blockDim.x) {
+            float4 v = buf[i];
+            v.x += 1.0f;
+            buf[i] = v;
+        }
+}
+__global__ void busy_spin(float* out, int iters) {
+    float a = threadIdx.x, b = 1.0001f;
+    for (int i = 0; i < iters; ++i) a = fmaf(a, b, 0.5f);
+    if (a == 12345.0f) out[0] = a;
+}
+
+int main(int argc, char** argv) {
+    const char* mode = argc > 1 ? argv[1] : "none";
     const int n = 128, ld = 128;
     std::vector<float> a(n * n);
     srand(1);
@@ -29,13 +49,37 @@ int main() {
     b.e[0] = LeafArgs{da, dx, dxt, info, ld, n, 0};
     cudaMemcpyToSymbol(g_probe, &stamps, sizeof(stamps));
     cudaEvent_t e0, e1; cudaEventCreate(&e0); cudaEventCreate(&e1);
-    for (int it = 0; it < 5; ++it) leaf_chol_inv_kernel<false><<<1, kLeafThreads, kLeafSmemBytes>>>(b);
-    cudaEventRecord(e0);
-    for (int it = 0; it < 20; ++it) leaf_chol_inv_kernel<false><<<1, kLeafThreads, kLeafSmemBytes>>>(b);
-    cudaEventRecord(e1);
+    cudaStream_t s0, s1;
+    cudaStreamCreateWithFlags(&s0, cudaStreamNonBlocking);
+    cudaStreamCreateWithFlags(&s1, cudaStreamNonBlocking);
+    float4* big = nullptr;
+    const size_t big_n4 = std::string(mode) == "l2" ? (32u << 20) / 16 : (1u << 30) / 16;
+    cudaMalloc(&big, big_n4 * 16);
+    cudaMemset(big, 0, big_n4 * 16);
+    auto busy = [&] {
+        if (std::string(mode) == "mem") busy_mem<<<147, 512, 0, s1>>>(big, big_n4, 1);
+        if (std::string(mode) == "l2") busy_mem<<<147, 512, 0, s1>>>(big, big_n4, 40);
+        if (std::string(mode) == "spin") busy_spin<<<147, 256, 0, s1>>>(reinterpret_cast<float*>(big), 400000);
+    };
+    for (int it = 0; it < 5; ++it) leaf_chol_inv_kernel<false><<<1, kLeafThreads, kLeafSmemBytes, s0>>>(b);
+    cudaDeviceSynchronize();
+    cudaEventRecord(e0, s0);
+    for (int it = 0; it < 20; ++it) leaf_chol_inv_kernel<false><<<1, kLeafThreads, kLeafSmemBytes, s0>>>(b);
+    cudaEventRecord(e1, s0);
     cudaDeviceSynchronize();
     float ms; cudaEventElapsedTime(&ms, e0, e1);
     printf("err=%s  avg %.2f us per launch (stream, back to back)\n", cudaGetErrorString(cudaGetLastError()), ms * 1000 / 20);
+    // last: one leaf launched while the busy kernel runs (its stamps are printed)
+    float busy_ms = 0;
+    for (int it = 0; it < 5; ++it) {
+        busy();
+        cudaEventRecord(e0, s0);
+        leaf_chol_inv_kernel<false><<<1, kLeafThreads, kLeafSmemBytes, s0>>>(b);
+        cudaEventRecord(e1, s0);
+        cudaDeviceSynchronize();
+        float t; cudaEventElapsedTime(&t, e0, e1); busy_ms += t;
+    }
+    printf("mode %s: %.2f us per leaf launched under load (event pair)\n", mode, busy_ms * 1000 / 5);
     long long h[64]; cudaMemcpy(h, stamps, sizeof(h), cudaMemcpyDeviceToHost);
     const char* names[] = {"start", "zero", "load", "p0A", "p0B", "p0C", "p1A", "p1B", "p1C",
                            "p2A", "p2B", "p2C", "p3A", "inv33", "x3", "", "", "", "", "store"};

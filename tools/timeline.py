@@ -103,7 +103,7 @@ def main():
     if os.environ.get("PF_TL_DUMP"):
         lo, hi = (int(v) for v in os.environ["PF_TL_DUMP"].split(":"))
         for e in by_end[lo:hi]:
-            print(f"  {e.name.split('(')[0][:28]:28s} start {e.time_range.start - t0:9.1f} end {e.time_range.end - t0:9.1f} dur {e.time_range.elapsed_us():7.1f}")
+            print(f"  {e.name.split('(')[0][:36]:36s} s{getattr(e, 'device_resource_id', -1):<4} start {e.time_range.start - t0:9.1f} end {e.time_range.end - t0:9.1f} dur {e.time_range.elapsed_us():7.1f}")
     print("marginal time by kernel (sum of end-to-end deltas):")
     for k, (n, t) in sorted(marg.items(), key=lambda x: -x[1][1]):
         print(f"  {k:40s} {n:5d} {t:9.1f} us  ({t / n:6.2f} us each)")
