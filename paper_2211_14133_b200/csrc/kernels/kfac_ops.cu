@@ -1302,6 +1302,14 @@ bool early_trtri_enabled() {  // PF_EARLY_TRTRI=0: whole TRTRI after the factori
     return on;
 }
 
+bool trtri_spine_enabled() {  // PF_TRTRI_SPINE=0: right subtree by levels after the factorisation (A/B)
+    static const bool on = [] {
+        const char* e = std::getenv("PF_TRTRI_SPINE");
+        return !(e && e[0] == '0');
+    }();
+    return on;
+}
+
 bool use_recursive_inverse(const std::vector<const pf_inverse_problem*>& probs) {
     static const int forced = [] {
         const char* e = std::getenv("PF_INV_RECURSIVE");
@@ -1341,42 +1349,71 @@ void damped_inverse_group(const std::vector<const pf_inverse_problem*>& probs, E
     if (recursive) {
         inverse_rec(ws, 0, d, em);
     } else {
-        // The TRTRI subtree of the root's left half [0, n1) needs only L and
-        // the leaves of panels < n1/128: it runs on a low-priority side stream
-        // under the rest of the factorisation (whose chain leaves most SMs
-        // idle); the right subtree and the root node follow the factorisation.
-        // (Streaming every finished node at its panel instead measured slower
-        // for the latency-bound calls: the many small nodes interfere with the
-        // chain; 2x4096 2.58 vs 2.53 ms.)
+        // TRTRI along the factorisation.  The node tree's right spine (the
+        // root, its right child, that node's right child, ...) is what the
+        // last panels finish; everything else is done before:
+        //   * the whole LEFT subtree of spine node (o, n1 | n2) needs only L
+        //     and the leaves of panels < (o + n1)/128: level-batched on a
+        //     low-priority side stream right after leaf (o + n1)/128 - 1;
+        //   * the node's first phase, T = L21 X11, needs L[o+n1:, o:o+n1]
+        //     (final once TRSM((o + n1)/128 - 1) ran, i.e. after leaf
+        //     (o + n1)/128) and X11: right after it on the same stream;
+        // so the tail after the last leaf is only the spine's X21 = -X22 T,
+        // deepest node first (2x4096: 8 level pairs + the root -> 5 pairs).
+        // PF_TRTRI_SPINE=0: only the root's left half and T early (the round-1
+        // schedule).  Streaming EVERY finished node at its own panel was
+        // measured slower (the many small nodes interfere with the chain).
         const int d = ws.front().d;
-        const int n1 = kTile * ((d + 2 * kTile - 1) / (2 * kTile));
-        std::vector<std::vector<TriNode>> left;
-        if (d > kLeaf) tri_height(n1, left, 0);
+        struct Spine {
+            TriNode node;
+            std::vector<std::vector<TriNode>> left;  // levels of its left subtree
+        };
+        std::vector<Spine> spine;
+        for (int o = 0, n = d; n > kLeaf;) {
+            const int n1 = kTile * ((n + 2 * kTile - 1) / (2 * kTile));
+            Spine sp{TriNode{o, n1, n - n1}, {}};
+            tri_height(n1, sp.left, o);
+            spine.push_back(std::move(sp));
+            if (!trtri_spine_enabled()) break;  // round-1 schedule: the root only
+            o += n1;
+            n -= n1;
+        }
         constexpr int evF = 29, evT = 30, kTrtriStream = 3;
-        const bool split = !left.empty() && early_trtri_enabled();
-        // The root's first phase, T = L21 X11, needs only L[n1:, 0:n1] (final
-        // once panel n1/128 - 1's TRSM is done) and X11: it follows the left
-        // subtree on the side stream, leaving only X21 = -X22 T after the
-        // right subtree.
-        const std::vector<std::vector<TriNode>> root{{TriNode{0, n1, d - n1}}};
-        // (emitted after leaf n1/128, i.e. after TRSM(n1/128 - 1) on the main
-        // stream, which writes the last block column of L21)
+        const bool early = !spine.empty() && early_trtri_enabled();
         cholesky_blocked(ws, em, [&](int k) {
-            const bool at_left = split && k == n1 / kLeaf - 1;
-            const bool at_root = split && early_root_enabled() && k == n1 / kLeaf;
-            if (!at_left && !at_root) return;
-            em.record(evF);
-            em.on(kTrtriStream);
-            em.wait(evF);
-            if (at_left) trtri_emit_levels(ws, em, left);
-            if (at_root) trtri_emit_levels(ws, em, root, 1);
-            em.record(evT);
-            em.on(0);
+            if (!early) return;
+            bool opened = false;
+            auto open = [&] {
+                if (opened) return;
+                opened = true;
+                em.record(evF);
+                em.on(kTrtriStream);
+                em.wait(evF);
+            };
+            for (const Spine& sp : spine) {
+                const int kl = (sp.node.o + sp.node.n1) / kLeaf - 1;
+                if (k == kl && !sp.left.empty()) {
+                    open();
+                    trtri_emit_levels(ws, em, sp.left);
+                }
+                if (k == kl + 1 && early_root_enabled()) {
+                    open();
+                    trtri_emit_levels(ws, em, {{sp.node}}, 1);
+                }
+            }
+            if (opened) {
+                em.record(evT);
+                em.on(0);
+            }
         });
-        if (split) {
-            em.wait(evT);  // s0 / s1 level slots are reused by the right subtree
-            trtri_levels(ws, em, n1, d - n1);
-            trtri_emit_levels(ws, em, root, early_root_enabled() ? 2 : 3);
+        if (early) {
+            em.wait(evT);  // level digit slots are reused below
+            if (!trtri_spine_enabled()) {  // round-1 schedule: right subtree by levels, then the root
+                const Spine& r = spine.front();
+                trtri_levels(ws, em, r.node.o + r.node.n1, r.node.n2);
+            }
+            for (auto it = spine.rbegin(); it != spine.rend(); ++it)
+                trtri_emit_levels(ws, em, {{it->node}}, early_root_enabled() ? 2 : 3);
         } else {
             trtri_levels(ws, em, 0, d);
         }
