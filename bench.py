@@ -664,6 +664,11 @@ def pipeline_section(args, rank, world, local_rank, dist):
         step = statistics.mean(r.step_ms for r in res)
         util = res[1].util
         info = {"refresh_period": t.refresh}
+        try:  # the paper's utilisation from kernel activity (CUPTI), beside the event-bracket one
+            from paper_2211_14133_b200.engine import kernel_activity
+            info["cupti"] = kernel_activity(t)
+        except Exception as e:  # profiler unavailable: reported, not fatal
+            info["cupti"] = {"error": f"{type(e).__name__}: {e}"[:200]}
         if t.filled is not None:
             m = S.schedule_metrics(t.filled.schedule)
             info["simulated_util"] = m[1] if isinstance(m, tuple) else getattr(m, "utilization", None)

@@ -109,6 +109,7 @@ class CudaBackend:
         self.losses: List[torch.Tensor] = []
         self.timeline: List[Tuple[str, torch.cuda.Event, torch.cuda.Event, dict]] = []
         self.record = False
+        self.recompute_on = bool(cfg.recompute)  # WorkKind::Recompute items in the program
         self.cur_step = 0  # set by the executor before each op (trace metadata)
 
     # ------------------------------------------------------------ timing helpers
@@ -145,14 +146,36 @@ class CudaBackend:
         else:
             inp = x.requires_grad_()
         mod.store.active_micro = micro if (capture and self.use_kfac) else None
-        out = mod(inp, pos, labels)
+        if self.recompute_on:
+            # activation recomputation: no autograd graph is kept between F and
+            # B, only the stage input; the Recompute op rebuilds it
+            with torch.no_grad():
+                out = mod(inp.detach() if not mod.is_first else inp, pos, labels)
+            self.saved[(stage, micro)] = (inp.detach() if not mod.is_first else inp, None)
+        else:
+            out = mod(inp, pos, labels)
+            self.saved[(stage, micro)] = (inp, out)
         mod.store.active_micro = None
-        self.saved[(stage, micro)] = (inp, out)
         self._end("F", e0, self.compute, stage=stage, micro_batch=micro)
         if mod.is_last:
             self.losses.append(out.detach())
             return None
         return out.detach().to(torch.bfloat16)
+
+    def recompute(self, stage, micro):
+        """WorkKind::Recompute: the micro-batch's forward again from its saved
+        stage input, now with autograd (the tapes were captured by the first
+        forward; this pass records none)."""
+        mod = self.stages[stage]
+        e0 = self._begin(self.compute)
+        ids, pos, labels = self.data[micro]
+        inp, _ = self.saved[(stage, micro)]
+        if not mod.is_first:
+            inp = inp.requires_grad_()
+        mod.store.active_micro = None
+        out = mod(inp, pos, labels)
+        self.saved[(stage, micro)] = (inp, out)
+        self._end("RECOMP", e0, self.compute, stage=stage, micro_batch=micro)
 
     def backward(self, stage, micro, gy, capture):
         mod = self.stages[stage]
@@ -392,6 +415,7 @@ def measure_stage_times(backend: "CudaBackend", reps: int = 3) -> MeasuredTimes:
     """Time the work items of this rank's first hosted stage.  Mutates the
     backend's model and K-FAC state: use a throw-away backend."""
     stage = min(backend.stages)
+    backend.recompute_on = False  # t_f and t_b as such; the schedule adds t_f per Recompute item
     mod, ks = backend.stages[stage], backend.kstate[stage]
     topo = backend.topo
     micro = next(m for m in range(topo.cfg.micro_batches)
@@ -487,7 +511,7 @@ class PipeFisherTrainer:
                                          S.AssignOptions(inversion_parallel=inversion_parallel))
             progs = R.device_programs(self.filled, cfg)  # inverse broadcast whenever W > 1
         if not kfac:
-            progs = [[o for o in p if o.kind in (R.F_, R.B_, R.SYNC_GRAD, R.PREC)] for p in progs]
+            progs = [[o for o in p if o.kind in (R.F_, R.RECOMP, R.B_, R.SYNC_GRAD, R.PREC)] for p in progs]
             for p in progs:
                 R._assign_gates(p)
         self.programs = progs
@@ -554,7 +578,48 @@ class PipeFisherTrainer:
                            busy, loss)
 
 
-_TRACE_KIND = {"F": S.WorkKind.Forward, "B": S.WorkKind.Backward, "CURV": S.WorkKind.Curvature,
+def kernel_activity(trainer: "PipeFisherTrainer") -> dict:
+    """One cycle under CUPTI (torch.profiler, CUDA activity only): the paper's
+    GPU utilisation -- the fraction of the cycle in which SOME kernel runs on
+    this device (reference definition over item intervals,
+    schedule.cpp:257-270) -- measured from kernel execution intervals instead
+    of the CUDA-event brackets of the ops (which cannot see host gaps inside
+    an op).  Also splits the kernel time into this library's K-FAC kernels
+    (pf::) and everything else (F/B, collectives, copies), and reports the
+    idle time.  Profiler numbers: for explanation, not for the bench value."""
+    from torch.profiler import ProfilerActivity, profile
+    torch.cuda.synchronize(trainer.device)
+    with profile(activities=[ProfilerActivity.CUDA]) as prof:
+        trainer.run_cycle()
+        torch.cuda.synchronize(trainer.device)
+    ev = [e for e in prof.events() if e.device_type.name == "CUDA" and e.time_range.elapsed_us() > 0]
+    if not ev:
+        return {"error": "no CUDA activity recorded"}
+    ev.sort(key=lambda e: e.time_range.start)
+    t0, t1 = ev[0].time_range.start, max(e.time_range.end for e in ev)
+    busy, cur_s, cur_e = 0.0, None, None
+    for e in ev:
+        a, b = e.time_range.start, e.time_range.end
+        if cur_s is None or a > cur_e:
+            if cur_s is not None:
+                busy += cur_e - cur_s
+            cur_s, cur_e = a, b
+        else:
+            cur_e = max(cur_e, b)
+    busy += cur_e - cur_s
+    kfac = sum(e.time_range.elapsed_us() for e in ev if "pf::" in e.name)
+    other = sum(e.time_range.elapsed_us() for e in ev if "pf::" not in e.name)
+    span = t1 - t0
+    steps = max(1, trainer.refresh)
+    return {"kernel_util": busy / span if span > 0 else 0.0, "span_ms": span / 1e3,
+            "idle_ms_per_step": (span - busy) / 1e3 / steps,
+            "kfac_kernel_ms_per_step": kfac / 1e3 / steps, "other_kernel_ms_per_step": other / 1e3 / steps,
+            "kernels": len(ev),
+            "definition": "union of CUDA kernel/memcpy execution intervals (CUPTI) / span of the cycle"}
+
+
+_TRACE_KIND = {"F": S.WorkKind.Forward, "B": S.WorkKind.Backward, "RECOMP": S.WorkKind.Recompute,
+               "CURV": S.WorkKind.Curvature,
                "INV": S.WorkKind.Inversion, "PREC": S.WorkKind.Precondition, "SYNC_GRAD": S.WorkKind.SyncGrad,
                "SYNC_CURV": S.WorkKind.SyncCurvature}
 

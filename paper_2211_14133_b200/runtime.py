@@ -49,8 +49,10 @@ from .schedule import Factor, Method, WorkKind
 
 # ---------------------------------------------------------------------- programs
 F_, B_, CURV, SYNC_CURV, INV, SYNC_GRAD, PREC = "F", "B", "CURV", "SYNC_CURV", "INV", "SYNC_GRAD", "PREC"
+RECOMP = "RECOMP"
+COMPUTE_OPS = (F_, RECOMP, B_)  # the compute stream's F/B work (K-FAC items gate on these)
 KFAC_STREAM_OPS = (CURV, SYNC_CURV, INV)
-_KIND = {WorkKind.Forward: F_, WorkKind.Backward: B_, WorkKind.Curvature: CURV,
+_KIND = {WorkKind.Forward: F_, WorkKind.Backward: B_, WorkKind.Recompute: RECOMP, WorkKind.Curvature: CURV,
          WorkKind.SyncCurvature: SYNC_CURV, WorkKind.Inversion: INV, WorkKind.SyncGrad: SYNC_GRAD,
          WorkKind.Precondition: PREC}
 
@@ -146,7 +148,7 @@ def device_programs(filled: S.FilledSchedule, cfg: S.PipelineConfig,
         for w in line:
             kind = _KIND.get(w.kind)
             if kind is None:
-                raise ValueError(f"runtime: unsupported work kind {w.kind!r} (recompute is not executed)")
+                raise ValueError(f"runtime: unsupported work kind {w.kind!r}")
             op = Op(kind, w.stage, w.step, w.start, w.duration, w.micro_batch, w.layer,
                     None if w.factor is None else int(w.factor))
             if kind in (F_, B_):
@@ -154,7 +156,7 @@ def device_programs(filled: S.FilledSchedule, cfg: S.PipelineConfig,
             if kind in (SYNC_CURV, SYNC_GRAD):
                 op.group = topo.replicas(w.stage)
             progs[dev].append(op)
-    rank = {k: i for i, k in enumerate((F_, B_, CURV, INV, SYNC_GRAD, PREC, SYNC_CURV))}
+    rank = {k: i for i, k in enumerate((F_, RECOMP, B_, CURV, INV, SYNC_GRAD, PREC, SYNC_CURV))}
     for p in progs:
         # stable: the assigner already sorted by (start, int(kind)); SyncGrad
         # must come before the Precondition of the same stage at equal start
@@ -251,16 +253,18 @@ def _canonicalize_collectives(progs: List[List[Op]], topo: Topology):
 def _assign_gates(p: List[Op]):
     last_fb = None
     for i, o in enumerate(p):
-        if o.kind in (F_, B_):
+        if o.kind in COMPUTE_OPS:
             last_fb = i
         elif o.kind in KFAC_STREAM_OPS or o.kind == "BCAST_INV":
             o.gate = last_fb
 
 
 def inline_program(cfg: S.PipelineConfig, refresh: int) -> List[Op]:
-    """D = 1, W = 1: no bubbles.  Step k of an R-step cycle: 1F1B order F/B,
-    then (k == 0) Curvature for every (layer, set, micro) and Inversion for
-    every (layer, set), then Precondition."""
+    """D = 1, W = 1: no bubbles.  Step k of an R-step cycle: 1F1B order F/B
+    (with cfg.recompute, a Recompute of the micro-batch glued in front of its
+    Backward, reference schedule.cpp:188-189, :215-223), then (k == 0)
+    Curvature for every (layer, set, micro) and Inversion for every
+    (layer, set), then Precondition."""
     if cfg.stages != 1:
         raise ValueError("inline_program is the single-stage (D = 1) case")
     n, L = cfg.micro_batches, cfg.layers_per_stage
@@ -268,6 +272,8 @@ def inline_program(cfg: S.PipelineConfig, refresh: int) -> List[Op]:
     t = 0.0
     for k in range(refresh):
         fb = [(F_, 0)] + [x for m in range(1, n) for x in ((B_, m - 1), (F_, m))] + [(B_, n - 1)]
+        if cfg.recompute:
+            fb = [x for kind, m in fb for x in (((RECOMP, m), (B_, m)) if kind == B_ else ((kind, m),))]
         for kind, m in fb:
             prog.append(Op(kind, 0, k, t, 1.0, m))
             t += 1.0
@@ -376,6 +382,12 @@ class Executor:
                 y = b.forward(op.stage, op.micro, x, capture=(op.step == 0), cycle=cycle)
                 if op.send:
                     comm.send(op.send, y)
+                fb_done[i - 1] = b.mark_compute()
+            elif op.kind == RECOMP:
+                # activation recomputation (reference WorkKind::Recompute): the
+                # forward of this micro-batch again, from its saved stage input,
+                # right before its backward on the same device
+                b.recompute(op.stage, op.micro)
                 fb_done[i - 1] = b.mark_compute()
             elif op.kind == B_:
                 gy = comm.recv(op.recv, b.act_shape(op.stage, op.micro)) if op.recv else None

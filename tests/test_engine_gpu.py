@@ -101,3 +101,31 @@ def test_measured_cost_table_closed_loop():
     assert t.costs.t_inv == pytest.approx(2 * m.inv) and t.costs.t_curv == m.curv
     r = t.run_cycle(record=True)
     assert torch.isfinite(torch.tensor(r.loss))
+
+
+def test_recompute_gives_the_same_training_step():
+    """Activation recomputation (reference WorkKind::Recompute, schedule.cpp:
+    188-189, :215-223): F keeps only the stage input, the Recompute op rebuilds
+    the graph right before B.  Same losses, tapes, factors and updated weights
+    as the run that keeps its activations (the recomputed forward is the same
+    arithmetic), and the program carries one Recompute per backward."""
+    from paper_2211_14133_b200 import runtime as R
+    from paper_2211_14133_b200.engine import PipeFisherTrainer
+    runs = []
+    for rc in (False, True):
+        cfg = S.PipelineConfig(stages=1, micro_batches=2, micro_batch_size=4, seq_len=64, layers_per_stage=2,
+                               recompute=rc)
+        t = PipeFisherTrainer(cfg, small(), kfac=True, refresh=2, damping=0.1, lr=1e-2, seed=3)
+        n_rec = sum(1 for o in t.program if o.kind == R.RECOMP)
+        assert n_rec == (2 * 2 if rc else 0)  # refresh 2 steps x 2 micro-batches
+        losses = [t.run_cycle().loss for _ in range(2)]
+        torch.cuda.synchronize()
+        ks = t.backend.kstate[0]
+        runs.append((losses, {k: v.clone() for k, v in ks.factor.items()},
+                     [p.detach().clone() for p in t.backend.stages[0].parameters()]))
+    (l0, f0, w0), (l1, f1, w1) = runs
+    assert l0 == l1
+    for k in f0:
+        assert torch.equal(f0[k], f1[k]), k
+    for a, b in zip(w0, w1):
+        assert torch.allclose(a, b, rtol=0, atol=1e-6)

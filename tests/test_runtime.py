@@ -25,9 +25,9 @@ CASES = [
 COSTS = S.CostTable(t_f=1.0, t_b=2.0, t_curv=0.05, t_inv=0.3, t_prec=0.1)
 
 
-def build(method, D, N, W, L, inv_par=False):
+def build(method, D, N, W, L, inv_par=False, recompute=False):
     cfg = S.PipelineConfig(method=method, stages=D, micro_batches=N, micro_batch_size=32,
-                           replicas=W, layers_per_stage=L)
+                           replicas=W, layers_per_stage=L, recompute=recompute)
     base = S.build_schedule(cfg, COSTS)
     filled = S.assign_works(base, cfg, COSTS, S.enumerate_kfac_works(cfg, COSTS),
                             S.AssignOptions(inversion_parallel=inv_par))
@@ -92,6 +92,29 @@ def test_kfac_dependencies_respected(name, method, D, N, W, L):
                 assert fbs, "precondition before the stage's backward"
 
 
+@pytest.mark.parametrize("method", [S.Method.GPipe, S.Method.OneF1B, S.Method.Chimera])
+def test_recompute_items_run_right_before_their_backward(method):
+    """With activation recomputation the reference schedule glues a Recompute
+    item (duration t_f) in front of every Backward on its device
+    (schedule.cpp:188-189, :215-223); the programs keep it there."""
+    cfg, filled, progs = build(method, 4, 4, 2 if method == S.Method.Chimera else 1, 2, recompute=True)
+    n_rec = 0
+    for dev, (p, line) in enumerate(zip(progs, filled.schedule.timelines)):
+        got = Counter(o.key() for o in p if not o.synthetic)
+        want = Counter((R._KIND[w.kind], w.stage, w.micro_batch, w.layer,
+                        None if w.factor is None else int(w.factor), w.step) for w in line)
+        assert got == want, dev
+        compute = [o for o in p if o.kind in R.COMPUTE_OPS]
+        for i, o in enumerate(compute):
+            if o.kind == R.B_:
+                prev = compute[i - 1]
+                assert (prev.kind, prev.stage, prev.micro, prev.step) == (R.RECOMP, o.stage, o.micro, o.step)
+                assert abs(prev.start + COSTS.t_f - o.start) < 1e-9
+                n_rec += 1
+    assert n_rec == sum(1 for p in progs for o in p if o.kind == R.RECOMP) > 0
+    R.check_channel_fifo(progs)
+
+
 def test_inline_program_single_device():
     cfg = S.PipelineConfig(stages=1, micro_batches=4, layers_per_stage=24)
     prog = R.inline_program(cfg, refresh=2)
@@ -103,6 +126,10 @@ def test_inline_program_single_device():
     assert fb == [(R.F_, 0), (R.B_, 0), (R.F_, 1), (R.B_, 1), (R.F_, 2), (R.B_, 2), (R.F_, 3), (R.B_, 3)]
     with pytest.raises(ValueError):
         R.inline_program(S.PipelineConfig(stages=2, micro_batches=2), 1)
+    rc = R.inline_program(S.PipelineConfig(stages=1, micro_batches=3, layers_per_stage=2, recompute=True), 1)
+    fb = [(o.kind, o.micro) for o in rc if o.kind in R.COMPUTE_OPS]
+    assert fb == [(R.F_, 0), (R.RECOMP, 0), (R.B_, 0), (R.F_, 1), (R.RECOMP, 1), (R.B_, 1),
+                  (R.F_, 2), (R.RECOMP, 2), (R.B_, 2)]
 
 
 # ---------------------------------------------------------------- real execution (gloo)
@@ -112,6 +139,7 @@ class RecordingBackend:
 
     def __init__(self, rank, topo):
         self.rank, self.topo = rank, topo
+        self.recompute_on = topo.cfg.recompute
         self.log = []
 
     def act_shape(self, stage, micro):
@@ -126,7 +154,12 @@ class RecordingBackend:
         self.log.append(("F", stage, micro))
         return torch.tensor([stage, micro, 0, cycle], dtype=torch.float32)
 
+    def recompute(self, stage, micro):
+        self.log.append(("RECOMP", stage, micro))
+
     def backward(self, stage, micro, gy, capture):
+        if self.recompute_on:  # the micro-batch's recompute ran right before
+            assert self.log[-1] == ("RECOMP", stage, micro), self.log[-3:]
         if stage < self.topo.D - 1:
             assert gy.tolist() == [stage + 1, micro, 1, 0], (stage, micro, gy)
         self.log.append(("B", stage, micro))
@@ -162,11 +195,11 @@ class RecordingBackend:
         pass
 
 
-def _worker(rank, world, port, method, D, N, W, L, inv_par, q):
+def _worker(rank, world, port, method, D, N, W, L, inv_par, q, recompute=False):
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
     dist.init_process_group("gloo", rank=rank, world_size=world)
     try:
-        cfg, filled, progs = build(method, D, N, W, L, inv_par)
+        cfg, filled, progs = build(method, D, N, W, L, inv_par, recompute)
         topo = R.Topology(cfg)
         comm = R.Comm(dist, rank, R.channel_plan(progs), [topo.replicas(s) for s in range(D)])
         be = RecordingBackend(rank, topo)
@@ -185,19 +218,21 @@ def _free_port():
         return s.getsockname()[1]
 
 
-@pytest.mark.parametrize("method,D,N,W,L,inv_par", [
-    (S.Method.GPipe, 2, 2, 1, 1, False),
-    (S.Method.OneF1B, 2, 4, 1, 2, False),
-    (S.Method.Chimera, 4, 4, 2, 1, False),   # world 4: both pipes, SyncCurvature + SyncGrad
-    (S.Method.GPipe, 2, 2, 2, 1, True),      # world 4: data-parallel replicas, inverse broadcast
+@pytest.mark.parametrize("method,D,N,W,L,inv_par,recompute", [
+    (S.Method.GPipe, 2, 2, 1, 1, False, False),
+    (S.Method.OneF1B, 2, 4, 1, 2, False, False),
+    (S.Method.Chimera, 4, 4, 2, 1, False, False),   # world 4: both pipes, SyncCurvature + SyncGrad
+    (S.Method.GPipe, 2, 2, 2, 1, True, False),      # world 4: data-parallel replicas, inverse broadcast
+    (S.Method.OneF1B, 2, 4, 1, 2, False, True),     # activation recomputation before every backward
 ])
-def test_gloo_execution_no_deadlock_and_data_routed(method, D, N, W, L, inv_par):
-    cfg = S.PipelineConfig(method=method, stages=D, micro_batches=N, replicas=W, layers_per_stage=L)
+def test_gloo_execution_no_deadlock_and_data_routed(method, D, N, W, L, inv_par, recompute):
+    cfg = S.PipelineConfig(method=method, stages=D, micro_batches=N, replicas=W, layers_per_stage=L,
+                           recompute=recompute)
     world = cfg.effective_devices()
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _free_port()
-    procs = [ctx.Process(target=_worker, args=(r, world, port, method, D, N, W, L, inv_par, q))
+    procs = [ctx.Process(target=_worker, args=(r, world, port, method, D, N, W, L, inv_par, q, recompute))
              for r in range(world)]
     for p in procs:
         p.start()
@@ -208,7 +243,7 @@ def test_gloo_execution_no_deadlock_and_data_routed(method, D, N, W, L, inv_par)
     for p in procs:
         p.join(timeout=60)
         assert p.exitcode == 0
-    _, _, progs = build(method, D, N, W, L, inv_par)
+    _, _, progs = build(method, D, N, W, L, inv_par, recompute)
     for r in range(world):
         n_ops = sum(1 for o in progs[r])
         assert len(logs[r]) == 2 * n_ops
