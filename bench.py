@@ -209,7 +209,9 @@ class LayerStep:
         self.tapes, self.factors, self.inv, self.digits = [], [], [], []
         for _, di, do in LINEARS:
             for d in (di, do):
-                self.tapes.append(torch.randn((d, TOKENS), generator=g, device="cuda").to(torch.bfloat16))
+                # token-major [tokens x d]: a layer's activations / output
+                # gradients as produced, read in place by the SYRK (MN-major)
+                self.tapes.append(torch.randn((TOKENS, d), generator=g, device="cuda").to(torch.bfloat16))
                 self.factors.append(torch.empty((d, d), device="cuda"))
                 self.inv.append(torch.empty((d, d), device="cuda"))
                 self.digits.append(torch.empty(K.slice_bytes(d, d), dtype=torch.uint8, device="cuda"))
@@ -217,7 +219,7 @@ class LayerStep:
         self.weights = [0.02 * torch.randn((do, di), generator=g, device="cuda") for _, di, do in LINEARS]
 
     def curvature(self):
-        self.K.syrk([(x, f, 1.0 / TOKENS, False) for x, f in zip(self.tapes, self.factors)],
+        self.K.syrk([(x, f, 1.0 / TOKENS, False, True) for x, f in zip(self.tapes, self.factors)],
                     fill_upper=False)
 
     def invert(self, which=None):

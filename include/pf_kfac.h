@@ -47,6 +47,12 @@ typedef struct pf_syrk_problem {
     int32_t d, n, ldx, ldf;
     float scale;
     int32_t accumulate;
+    /* 0: x is feature-major [d x n] (examples contiguous, the reference's
+     *    BatchTape layout, kfac.hpp:33-37), ldx >= n;
+     * 1: x is token-major [n x d] (features contiguous: a layer's activations
+     *    or output gradients as the forward/backward produce them), ldx >= d;
+     *    read in place, no transposed copy.  Either way ldx % 8 == 0. */
+    int32_t layout;
 } pf_syrk_problem;
 
 /* fill_upper = 1 writes the full symmetric matrix (reference semantics);

@@ -53,7 +53,7 @@ class PfStaleness(C.Structure):
 class PfSyrkProblem(C.Structure):
     _fields_ = [("x", C.c_void_p), ("f", C.c_void_p), ("d", C.c_int32), ("n", C.c_int32),
                 ("ldx", C.c_int32), ("ldf", C.c_int32), ("scale", C.c_float),
-                ("accumulate", C.c_int32)]
+                ("accumulate", C.c_int32), ("layout", C.c_int32)]
 
 
 class PfInverseProblem(C.Structure):

@@ -6,7 +6,8 @@ hot-path kernel of this repo.  What matters for the K-FAC path is the tape
 capture: every K-FAC linear (Q, K, V, O, FFN1, FFN2 of each encoder layer)
 records its input ``a`` and output gradient ``e`` for the micro-batches of
 the refresh cycle's first step (reference BatchTape, kfac.hpp:33-37; SURVEY
-A.5), as bf16 ``[d x n_tokens]`` — the K-major SYRK operand.  Q/K/V share one
+A.5), as bf16 ``[n_tokens x d]`` exactly as the forward / backward produce
+it — the SYRK reads it in place as an MN-major operand (no transpose).  Q/K/V share one
 input, so the A-set of a layer has 4 distinct tapes for 6 factors.
 
 A stage owns a contiguous run of encoder layers, plus the embeddings (first
@@ -58,8 +59,15 @@ class TapeStore:
     def put(self, layer: int, key: str, x2d: torch.Tensor):
         if self.active_micro is None:
             return
-        # [n x d] activations -> [d x n] tape (tokens contiguous: the SYRK's K-major operand)
-        self.tapes[(layer, key, self.active_micro)] = x2d.detach().to(torch.bfloat16).t().contiguous()
+        # token-major [n x d] as produced (features contiguous): the SYRK reads
+        # it in place as an MN-major tensor-core operand -- no transposed copy
+        # (a view of the bf16 activation when it already is one)
+        x2d = x2d.detach()
+        if x2d.dtype != torch.bfloat16:
+            x2d = x2d.to(torch.bfloat16)
+        if x2d.stride(1) != 1 or x2d.stride(0) % 8 != 0 or x2d.data_ptr() % 16 != 0:
+            x2d = x2d.contiguous()
+        self.tapes[(layer, key, self.active_micro)] = x2d
 
     def get(self, layer: int, key: str, micro: int) -> torch.Tensor:
         return self.tapes[(layer, key, micro)]

@@ -152,7 +152,7 @@ std::vector<std::pair<Matrix, Matrix>> factors_for(const BatchTape& tape, const 
             continue;
         }
         probs.push_back(pf_syrk_problem{tapes[i].buf.p, outs[i].f(), tapes[i].d, tapes[i].n, tapes[i].ld,
-                                        outs[i].ld, scale, 0});
+                                        outs[i].ld, scale, 0, 0});
     }
     if (!probs.empty())
         pf_check(pf_curvature_syrk_grouped(probs.data(), static_cast<int>(probs.size()), 1, stream()),

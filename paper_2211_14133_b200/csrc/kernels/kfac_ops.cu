@@ -149,6 +149,21 @@ void encode(CUtensorMap* m, const void* ptr, bool bf16, int rows, int k, size_t 
     if (r != CUDA_SUCCESS) throw CudaError("cuTensorMapEncodeTiled failed: " + std::to_string(r));
 }
 
+// MN-major bf16 operand [k x rows] (rows contiguous, pitch per k): dims
+// {rows, k}, box {64, 64}; a 128-row tile is two boxes (umma_gemm.cuh).
+void encode_mn(CUtensorMap* m, const void* ptr, int rows, int k, size_t pitch_bytes) {
+    if (!aligned16(ptr) || pitch_bytes % 16 != 0)
+        throw std::invalid_argument("TMA operand needs 16-byte aligned base and row pitch");
+    const cuuint64_t dims[2] = {static_cast<cuuint64_t>(rows), static_cast<cuuint64_t>(k)};
+    const cuuint64_t strides[1] = {static_cast<cuuint64_t>(pitch_bytes)};
+    const cuuint32_t box[2] = {64, 64};
+    const cuuint32_t estr[2] = {1, 1};
+    const CUresult r = encoder()(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(ptr), dims, strides, box,
+                                 estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                                 CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r != CUDA_SUCCESS) throw CudaError("cuTensorMapEncodeTiled(mn) failed: " + std::to_string(r));
+}
+
 // 3-D map over the 4 digit planes of a sliced operand: dims {k, rows, plane},
 // box {64, 128, 4} (one TMA per operand tile per k-block).
 void encode_planes(CUtensorMap* m, const int8_t* planes, int rows, int k, int kpad, int64_t plane_stride,
@@ -282,6 +297,7 @@ struct GemmSpec {
     const float* aux = nullptr;  // EPI_DIAG_SPLIT: X and X^T
     const float* aux_t = nullptr;
     int ld_aux = 0;
+    bool mn_major = false;  // kBF16: a_bf16 / b_bf16 are [k x rows] with pitch lda / ldb
 };
 
 // GemmSpec -> GemmDesc, encoding its operand tensor maps at maps[*n_maps...]
@@ -294,8 +310,12 @@ int make_desc(const GemmSpec& s, GemmDesc& d, CUtensorMap* maps, int n_maps) {
     auto put_maps = [&](bool is_a) {
         const int first = m;
         if constexpr (kFmt == kBF16) {
-            encode(&maps[m++], is_a ? s.a_bf16 : s.b_bf16, true, is_a ? s.rows : s.cols, s.k,
-                   static_cast<size_t>(is_a ? s.lda : s.ldb) * 2);
+            if (s.mn_major)
+                encode_mn(&maps[m++], is_a ? s.a_bf16 : s.b_bf16, is_a ? s.rows : s.cols, s.k,
+                          static_cast<size_t>(is_a ? s.lda : s.ldb) * 2);
+            else
+                encode(&maps[m++], is_a ? s.a_bf16 : s.b_bf16, true, is_a ? s.rows : s.cols, s.k,
+                       static_cast<size_t>(is_a ? s.lda : s.ldb) * 2);
         } else {
             const Sliced& o = is_a ? s.a : s.b;
             encode_planes(&maps[m++], o.planes, o.rows, o.k, o.kpad, o.plane_stride, is_a ? kTile : kN);
@@ -326,6 +346,7 @@ int make_desc(const GemmSpec& s, GemmDesc& d, CUtensorMap* maps, int n_maps) {
     d.aux = s.aux;
     d.aux_t = s.aux_t;
     d.ld_aux = s.ld_aux;
+    d.mn_major = kFmt == kBF16 && s.mn_major ? 1 : 0;
     (void)sizeof(T);
     return m - n_maps;
 }
@@ -1648,11 +1669,14 @@ int pf_curvature_syrk_grouped(const pf_syrk_problem* problems, int count, int fi
         std::vector<GemmSpec> specs;
         for (int i = 0; i < count; ++i) {
             const pf_syrk_problem& p = problems[i];
-            if (p.d < 1 || p.n < 1 || p.ldx < p.n || p.ldf < p.d || !p.x || !p.f)
+            if (p.layout != 0 && p.layout != 1) throw std::invalid_argument("curvature_syrk: bad layout");
+            const bool tm = p.layout == 1;  // token-major x [n x d]
+            if (p.d < 1 || p.n < 1 || p.ldx < (tm ? p.d : p.n) || p.ldf < p.d || !p.x || !p.f)
                 throw ShapeError("curvature_syrk: shape mismatch");
             if (p.ldx % 8 != 0 || !aligned16(p.x))
                 throw ShapeError("curvature_syrk: x needs 16-byte rows (ldx % 8 == 0)");
             GemmSpec s;
+            s.mn_major = tm;
             s.a_bf16 = s.b_bf16 = p.x;
             s.lda = s.ldb = p.ldx;
             s.rows = s.cols = p.d;
@@ -1673,7 +1697,7 @@ int pf_curvature_syrk_grouped(const pf_syrk_problem* problems, int count, int fi
 
 int pf_curvature_syrk(const void* x_bf16, int d, int n, int ldx, float scale, int accumulate,
                       float* f, int ldf, int fill_upper, void* stream) {
-    pf_syrk_problem p{x_bf16, f, d, n, ldx, ldf, scale, accumulate};
+    pf_syrk_problem p{x_bf16, f, d, n, ldx, ldf, scale, accumulate, 0};
     return pf_curvature_syrk_grouped(&p, 1, fill_upper, stream);
 }
 

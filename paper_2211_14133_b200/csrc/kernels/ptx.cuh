@@ -251,6 +251,25 @@ __device__ __forceinline__ uint64_t sw64_kmajor_desc(uint32_t smem_addr) {
     return d;
 }
 
+// MN-major (feature-contiguous) operand tile with SWIZZLE_128B, as TMA
+// writes a box of {64 MN elements, K rows}: 128-B rows along K, 8-row
+// (1024 B) swizzle atoms; LBO = byte stride between the 64-element MN blocks,
+// SBO = byte stride between 8-row K groups (canonical MN-major SW128 layout
+// ((T,8,m),(8,k)) : ((1,T,LBO),(8T,SBO)), T = 8 bf16 per 16 B).
+__device__ __forceinline__ uint64_t sw128_mnmajor_desc(uint32_t smem_addr, uint32_t lbo_bytes,
+                                                       uint32_t sbo_bytes) {
+    uint64_t d = 0;
+    d |= static_cast<uint64_t>((smem_addr & 0x3FFFFu) >> 4);
+    d |= static_cast<uint64_t>((lbo_bytes >> 4) & 0x3FFFu) << 16;
+    d |= static_cast<uint64_t>((sbo_bytes >> 4) & 0x3FFFu) << 32;
+    d |= static_cast<uint64_t>(1u) << 46;            // version
+    d |= static_cast<uint64_t>(2u) << 61;            // SWIZZLE_128B
+    return d;
+}
+// instruction-descriptor bits: A / B read MN-major ("transposed")
+constexpr uint32_t kIdescAMnMajor = 1u << 15;
+constexpr uint32_t kIdescBMnMajor = 1u << 16;
+
 // Instruction descriptor: fp32 accumulate, K-major A and B, MxN tile.
 // fmt: 1 = BF16 (kind::f16), 2 = TF32 (kind::tf32).
 __host__ __device__ constexpr uint32_t make_idesc(uint32_t fmt, uint32_t m, uint32_t n) {

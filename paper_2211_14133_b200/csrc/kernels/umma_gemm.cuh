@@ -115,6 +115,8 @@ struct GemmDesc {
     const float* aux;    // EPI_DIAG_SPLIT: X (16-byte aligned rows, ld_aux % 4 == 0)
     const float* aux_t;  //   and X^T (same ld)
     int ld_aux;
+    int mn_major;        // kBF16: operands stored [k x rows] (row-contiguous, e.g. token-major
+                         // activations [tokens x features]); two 64-wide TMA boxes per tile
 };
 
 struct GemmBatch {
@@ -517,6 +519,12 @@ __global__ void __launch_bounds__(GemmTraits<kFmt, kN>::kThreads, GemmTraits<kFm
             if constexpr (kFmt == kOZ8) {
                 ptx::tma_load_3d(a_plane(s, 0), &batch.maps[P.a_map], &full[s], kc, tm * kTile, 0);
                 ptx::tma_load_3d(b_plane(s, 0), &batch.maps[P.b_map], &full[s], kc, tn * kN, 0);
+            } else if (P.mn_major) {
+                // box {64 features, 64 tokens} per half: [half][token][64 features]
+                ptx::tma_load_2d(a_plane(s, 0), &batch.maps[P.a_map], &full[s], tm * kTile, kc);
+                ptx::tma_load_2d(a_plane(s, 0) + T::kPlaneBytes / 2, &batch.maps[P.a_map], &full[s], tm * kTile + 64, kc);
+                ptx::tma_load_2d(b_plane(s, 0), &batch.maps[P.b_map], &full[s], tn * kN, kc);
+                ptx::tma_load_2d(b_plane(s, 0) + T::kPlaneBytesB / 2, &batch.maps[P.b_map], &full[s], tn * kN + 64, kc);
             } else {
                 ptx::tma_load_2d(a_plane(s, 0), &batch.maps[P.a_map], &full[s], kc, tm * kTile);
                 ptx::tma_load_2d(b_plane(s, 0), &batch.maps[P.b_map], &full[s], kc, tn * kN);
@@ -550,6 +558,14 @@ __global__ void __launch_bounds__(GemmTraits<kFmt, kN>::kThreads, GemmTraits<kFm
                             started |= 1u << g;
                         }
                     }
+                } else if (P.mn_major) {
+                    // 16 K rows per UMMA = two 8-row groups of 1024 B
+                    const uint32_t moff = ks * 2048;
+                    ptx::umma_f16(tmem,
+                                  ptx::sw128_mnmajor_desc(ptx::smem_u32(a_plane(s, 0)) + moff, T::kPlaneBytes / 2, 1024),
+                                  ptx::sw128_mnmajor_desc(ptx::smem_u32(b_plane(s, 0)) + moff, T::kPlaneBytesB / 2, 1024),
+                                  T::kIdesc | ptx::kIdescAMnMajor | ptx::kIdescBMnMajor, started);
+                    started = 1;
                 } else {
                     ptx::umma_f16(tmem, ptx::sw128_kmajor_desc(ptx::smem_u32(a_plane(s, 0)) + off),
                                   ptx::sw128_kmajor_desc(ptx::smem_u32(b_plane(s, 0)) + off),

@@ -214,7 +214,7 @@ class CudaBackend:
                 for key in ks.keys(f):
                     x = mod.store.get(layer, key, micro)
                     x.record_stream(self.kfac_stream)
-                    probs.append((x, ks.factor[(layer, key)], scale, ks.started[(layer, f)]))
+                    probs.append((x, ks.factor[(layer, key)], scale, ks.started[(layer, f)], True))  # token-major
                     pending.add((stage, layer, key))
                 ks.started[(layer, f)] = True
             if probs:

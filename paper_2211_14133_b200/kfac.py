@@ -108,19 +108,27 @@ def to_tape_layout(x: torch.Tensor) -> torch.Tensor:
 
 
 # ------------------------------------------------------------------ curvature
-def syrk(problems: Sequence[Tuple[torch.Tensor, torch.Tensor, float, bool]],
-         fill_upper: bool = True) -> None:
-    """Grouped F = scale * X X^T (+F).  problems: (x_bf16 [d x n], f_fp32 [d x d], scale, accumulate)."""
+def syrk(problems: Sequence[Tuple], fill_upper: bool = True) -> None:
+    """Grouped F = scale * X X^T (+F).  problems: (x_bf16, f_fp32 [d x d],
+    scale, accumulate[, token_major]).  x is [d x n] (examples contiguous,
+    the BatchTape layout) or, with token_major=True, [n x d] -- a layer's
+    activations / output gradients as produced (features contiguous), read
+    in place by the tensor cores (MN-major operand), no transposed copy."""
     arr = (L.PfSyrkProblem * len(problems))()
-    for i, (x, f, scale, acc) in enumerate(problems):
+    for i, prob in enumerate(problems):
+        x, f, scale, acc = prob[:4]
+        tm = bool(prob[4]) if len(prob) > 4 else False
         _require_device(x, "syrk x")
         _require_device(f, "syrk f")
         if x.dtype != torch.bfloat16 or f.dtype != torch.float32:
             raise ValueError("syrk: x must be bf16 and f fp32")
-        if f.shape != (x.shape[0], x.shape[0]) or f.stride(1) != 1 or x.stride(1) != 1:
+        if x.dim() != 2 or x.stride(1) != 1 or f.stride(1) != 1:
+            raise ValueError("syrk: x and f need contiguous rows")
+        d, n = (x.shape[1], x.shape[0]) if tm else (x.shape[0], x.shape[1])
+        if f.shape != (d, d):
             raise ValueError("syrk: shape mismatch")
-        arr[i] = L.PfSyrkProblem(x.data_ptr(), f.data_ptr(), x.shape[0], x.shape[1], x.stride(0),
-                                 f.stride(0), float(scale), int(bool(acc)))
+        arr[i] = L.PfSyrkProblem(x.data_ptr(), f.data_ptr(), d, n, x.stride(0), f.stride(0), float(scale),
+                                 int(bool(acc)), 1 if tm else 0)
     L.check(L.lib().pf_curvature_syrk_grouped(arr, len(problems), int(fill_upper), _stream()),
             "curvature_syrk")
 

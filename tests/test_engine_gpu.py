@@ -52,7 +52,8 @@ def test_curvature_accumulates_micro_batches_like_the_reference():
     ks = b.kstate[0]
     for l in range(2):
         for key in ("a_qkv", "a_ffn2", "e_q", "e_ffn1"):
-            want = sum(tapes[(l, key, m)].double() @ tapes[(l, key, m)].double().T for m in range(2)) / n
+            # tapes are token-major [n x d] (read in place by the SYRK)
+            want = sum(tapes[(l, key, m)].double().T @ tapes[(l, key, m)].double() for m in range(2)) / n
             got = torch.tril(ks.factor[(l, key)].double())
             assert rel(got, torch.tril(want)) < 1e-3, (l, key)
 

@@ -381,3 +381,42 @@ def test_large_batch_uses_recursive_schedule_and_matches_oracle(K):
         got = o.double().cpu().numpy()
         assert rel_fro(got, R.orc_cholesky_spd_inverse(m32, 0.1)) <= 1e-4
         assert residual(m32, got, 0.1) <= INV_RESIDUAL_TOL
+
+
+@pytest.mark.parametrize("d,n", [(64, 96), (128, 128), (200, 72), (256, 512), (1024, 4096), (4096, 512)])
+def test_syrk_token_major_matches_feature_major(K, d, n):
+    """Token-major tapes ([n x d], a layer's activations as produced) are read
+    in place as MN-major tensor-core operands: the factor is bit-identical to
+    the feature-major call on the transposed copy (same bf16 products, same
+    fp32 accumulation order per tile), and matches the oracle."""
+    g = torch.Generator(device="cuda").manual_seed(d * 7 + n)
+    xt = torch.randn((n, (d + 7) // 8 * 8), generator=g, device="cuda").to(torch.bfloat16)[:, :d]
+    x = xt.t().contiguous()
+    if n % 8:
+        x = K.to_tape_layout(x)
+    f_km = torch.empty((d, d), device="cuda")
+    f_mn = torch.empty((d, d), device="cuda")
+    K.syrk([(x, f_km, 1.0 / n, False)], fill_upper=True)
+    K.syrk([(xt, f_mn, 1.0 / n, False, True)], fill_upper=True)
+    torch.cuda.synchronize()
+    assert torch.equal(f_km, f_mn)
+    if d <= 256:
+        want = R.orc_curvature_factor(x.double().cpu().numpy()[:, :n])
+        got = f_mn.double().cpu().numpy()
+        assert np.linalg.norm(got - want) / np.linalg.norm(want) < 1e-3
+
+
+def test_syrk_token_major_grouped_accumulate_with_padded_rows(K):
+    """Grouped token-major problems with a row pitch wider than d (a view of a
+    wider activation buffer) and accumulate=True."""
+    g = torch.Generator(device="cuda").manual_seed(5)
+    buf = torch.randn((512, 1040), generator=g, device="cuda").to(torch.bfloat16)
+    a, b = buf[:, :1024], buf[:, 8:8 + 384]
+    fa = torch.zeros((1024, 1024), device="cuda")
+    fb = torch.full((384, 384), 0.5, device="cuda")
+    K.syrk([(a, fa, 1.0, False, True), (b, fb, 2.0, True, True)], fill_upper=True)
+    torch.cuda.synchronize()
+    wa = a.float().t() @ a.float()
+    wb = 0.5 + 2.0 * (b.float().t() @ b.float())
+    assert ((fa - wa).norm() / wa.norm()).item() < 1e-5
+    assert ((fb - wb).norm() / wb.norm()).item() < 1e-5
