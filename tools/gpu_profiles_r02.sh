@@ -1,0 +1,32 @@
+#!/bin/bash
+# Round-2 evidence pass: bench line, launch list of one layer step, and one
+# `ncu --set full` capture of every kernel class of the layer step (SYRK,
+# persistent digit GEMM, the three split widths of the short-K digit GEMM,
+# leaf, short / long slicer, damp).  Usage:
+#   gpurun --timeout 3000 -- 'bash tools/gpu_profiles_r02.sh <tag>'
+set -u
+TAG=${1:-r02}
+OUT=gpurun_out/$TAG; mkdir -p $OUT
+run() { echo "== $*" >> $OUT/log.txt; "$@" >> $OUT/log.txt 2>&1; echo "rc=$?" >> $OUT/log.txt; }
+nvidia-smi > $OUT/nvidia-smi.txt 2>&1
+nproc > $OUT/host.txt; lscpu | grep -E 'Model name|^CPU\(s\)' >> $OUT/host.txt
+[ "${SKIP_TESTS:-0}" = 1 ] || run timeout 900 python -m pytest tests -m gpu -x -q
+run timeout 900 python bench.py --steps 20 --warmup 5
+grep '^{' $OUT/log.txt | tail -1 > $OUT/bench.json
+run timeout 300 ncu --profile-from-start off --metrics gpu__time_duration.sum --clock-control none --csv \
+    --log-file $OUT/launches.csv python tools/prof_phase.py step 2
+cap() {  # name phase kernel-regex skip
+  run timeout 600 ncu --profile-from-start off --set full --clock-control none --import-source on --kernel-name-base demangled \
+      -k "regex:$3" -s ${4:-0} -c 1 -o $OUT/$1 python tools/prof_phase.py $2 1
+}
+cap syrk curvature 'umma_gemm_kernel<1'
+cap prec precondition 'umma_gemm_persist'
+cap gemm32 inversion 'umma_gemm_kernel<3, 32' 20
+cap gemm64 inversion 'umma_gemm_kernel<3, 64' 10
+cap gemm128 inversion 'umma_gemm_kernel<3, 128' 10
+cap leaf inversion 'leaf_chol' 10
+cap slice_short inversion 'slice_short' 20
+cap slice_long inversion 'slice_long'
+cap damp inversion 'damp_kernel'
+cap lauum inversion 'umma_gemm_persist_kernel<true' 
+echo finished >> $OUT/log.txt

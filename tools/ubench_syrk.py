@@ -37,7 +37,7 @@ def timed(fn, iters=20):
 
 def main():
     torch.cuda.set_device(0)
-    cases = [[(256, 4096)], [(512, 4096)], [(1024, 4096)], [(2048, 4096)], [(4096, 4096)],
+    cases = [[(128, 64)], [(128, 512)], [(128, 4096)], [(256, 4096)], [(512, 4096)], [(1024, 4096)], [(2048, 4096)], [(4096, 4096)],
              [(1024, 4096)] * 10 + [(4096, 4096)] * 2]
     for spec in cases:
         xs_f = [torch.randn((d, n), device="cuda").to(torch.bfloat16) for d, n in spec]
