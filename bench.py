@@ -650,7 +650,7 @@ def pipeline_section(args, rank, world, local_rank, dist):
 
     def measure(kfac):
         t = PipeFisherTrainer(cfg, bert, rank, world, torch.device("cuda", local_rank), kfac=kfac,
-                              refresh=2, costs=costs_box["costs"], dist=dist, seed=11)
+                              refresh=2, costs=costs_box["costs"], dist=dist, seed=11, graph_fb=True)
         if t.measured is not None:
             m = t.measured
             t_meas["times"] = m
@@ -690,7 +690,8 @@ def pipeline_section(args, rank, world, local_rank, dist):
         out.update({"step_ms": step_ms, "plain_step_ms": plain_ms, "step_ratio_vs_plain": step_ms / plain_ms,
                     "gpu_util": util, "plain_gpu_util": plain_util,
                     "sequences_per_s": seqs / (step_ms * 1e-3), "loss": loss, **info,
-                    "util_definition": "union of F/B/K-FAC/collective op intervals (CUDA events) / cycle wall time, min over ranks"})
+                    "util_definition": "union of F/B/K-FAC/collective op intervals (CUDA events) / cycle wall time, min over ranks; cupti.kernel_util = union of kernel execution intervals (the paper's definition)",
+                    "fb": "BERT F/B of every (stage, micro-batch, tape capture) replayed as CUDA graphs (engine graph_fb)"})
         if "measured" in costs_box:
             out["measured_costs"] = costs_box["measured"]
         if world == 1 and t_meas.get("times") is not None:

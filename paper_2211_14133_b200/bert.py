@@ -156,7 +156,8 @@ class BertStage(nn.Module):
     def forward(self, x, mlm_positions=None, mlm_labels=None):
         """First stage: x = token ids [B, S]; others: hidden [B, S, h].
         Last stage returns the scalar MLM loss, others the hidden state."""
-        with torch.autocast("cuda", dtype=torch.bfloat16, enabled=x.is_cuda):
+        # (no autocast weight cache: the stage may be captured into CUDA graphs)
+        with torch.autocast("cuda", dtype=torch.bfloat16, enabled=x.is_cuda, cache_enabled=False):
             if self.is_first:
                 pos = torch.arange(x.shape[1], device=x.device)
                 x = self.ln_emb(self.tok(x) + self.pos(pos)[None])

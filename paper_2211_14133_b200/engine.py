@@ -72,9 +72,20 @@ def _tril_index(d: int, device) -> torch.Tensor:
     return _TRIL[key]
 
 
+class _StageCall(torch.nn.Module):
+    """One graphed F/B key of a stage (the stage module is shared)."""
+
+    def __init__(self, stage: torch.nn.Module):
+        super().__init__()
+        self.stage = stage
+
+    def forward(self, x, mlm_positions, mlm_labels):
+        return self.stage(x, mlm_positions, mlm_labels)
+
+
 class CudaBackend:
     def __init__(self, topo: R.Topology, bert: BertConfig, rank: int, device, kfac: bool = True,
-                 damping: float = 0.1, lr: float = 1e-3, seed: int = 0, dist=None):
+                 damping: float = 0.1, lr: float = 1e-3, seed: int = 0, dist=None, graph_fb: bool = False):
         cfg = topo.cfg
         if dist is None:
             import torch.distributed as dist
@@ -110,6 +121,14 @@ class CudaBackend:
         self.timeline: List[Tuple[str, torch.cuda.Event, torch.cuda.Event, dict]] = []
         self.record = False
         self.recompute_on = bool(cfg.recompute)  # WorkKind::Recompute items in the program
+        # F/B of each (stage, micro-batch, tape capture) as CUDA graphs
+        # (torch.cuda.make_graphed_callables): the eager BERT F/B is host-bound
+        # (CUPTI kernel utilisation ~0.65 at D = 1).  One graph pair per key, so
+        # the step-0 tapes (views of graph-static activations / gradients) stay
+        # valid until that key replays in the next refresh cycle, after the
+        # cycle-end join with the K-FAC stream.
+        self.graph_fb = bool(graph_fb) and not self.recompute_on
+        self.graphed: Dict[Tuple[int, int, bool], object] = {}
         self.cur_step = 0  # set by the executor before each op (trace metadata)
 
     # ------------------------------------------------------------ timing helpers
@@ -146,7 +165,27 @@ class CudaBackend:
         else:
             inp = x.requires_grad_()
         mod.store.active_micro = micro if (capture and self.use_kfac) else None
-        if self.recompute_on:
+        if self.graph_fb:
+            key = (stage, micro, bool(capture and self.use_kfac))
+            fn = self.graphed.get(key)
+            if fn is None:
+                # warm-up + capture run the forward / backward on sample inputs
+                # (tapes recorded during the capture are the graph's static
+                # tensors); parameters' .grad are untouched by the capture
+                sample = inp.detach().clone().requires_grad_(not mod.is_first) if not mod.is_first else inp
+                # a wrapper per key: make_graphed_callables replaces the forward
+                # of the module it is given (its parameters are the stage's)
+                fn = torch.cuda.make_graphed_callables(_StageCall(mod), (sample, pos, labels),
+                                                       allow_unused_input=True)
+                # the capture recorded this key's tapes (forward AND backward):
+                # graph-static tensors, re-registered at every replay
+                tapes = {k: v for k, v in mod.store.tapes.items() if key[2] and k[2] == micro}
+                self.graphed[key] = (fn, tapes)
+            fn, tapes = self.graphed[key]
+            mod.store.tapes.update(tapes)
+            out = fn(inp, pos, labels)
+            self.saved[(stage, micro)] = (inp, out)
+        elif self.recompute_on:
             # activation recomputation: no autograd graph is kept between F and
             # B, only the stage input; the Recompute op rebuilds it
             with torch.no_grad():
@@ -487,19 +526,21 @@ class PipeFisherTrainer:
     def __init__(self, cfg: S.PipelineConfig, bert: BertConfig, rank: int = 0, world: int = 1,
                  device=None, kfac: bool = True, refresh: int = 2, costs: Optional[S.CostTable] = None,
                  damping: float = 0.1, lr: float = 1e-3, seed: int = 0, dist=None,
-                 inversion_parallel: bool = False):
+                 inversion_parallel: bool = False, graph_fb: bool = False):
         self.cfg, self.bert, self.rank, self.world = cfg, bert, rank, world
         self.topo = R.Topology(cfg)
         if self.topo.n_devices() != world:
             raise ValueError(f"config needs {self.topo.n_devices()} devices, world is {world}")
         self.device = device or torch.device("cuda", torch.cuda.current_device())
         self.measured: Optional[MeasuredTimes] = None
+        self._graph_fb = graph_fb
         if isinstance(costs, str):
             if costs != "measured":
                 raise ValueError("costs: a CostTable or 'measured'")
             costs = self._measure_costs(damping, lr, seed, dist)
         self.costs = costs
-        self.backend = CudaBackend(self.topo, bert, rank, self.device, kfac, damping, lr, seed, dist)
+        self.backend = CudaBackend(self.topo, bert, rank, self.device, kfac, damping, lr, seed, dist,
+                                   graph_fb=graph_fb)
         self.filled = None
         if cfg.stages == 1 and cfg.replicas == 1:
             prog = R.inline_program(cfg, refresh)
@@ -530,7 +571,8 @@ class PipeFisherTrainer:
         items on a throw-away backend, take the max over ranks (every rank
         must build the identical schedule), convert to the reference's
         cost-table semantics."""
-        probe = CudaBackend(self.topo, self.bert, self.rank, self.device, True, damping, lr, seed, dist)
+        probe = CudaBackend(self.topo, self.bert, self.rank, self.device, True, damping, lr, seed, dist,
+                            graph_fb=self._graph_fb)
         t = measure_stage_times(probe)
         del probe
         torch.cuda.empty_cache()

@@ -130,3 +130,27 @@ def test_recompute_gives_the_same_training_step():
         assert torch.equal(f0[k], f1[k]), k
     for a, b in zip(w0, w1):
         assert torch.allclose(a, b, rtol=0, atol=1e-6)
+
+
+def test_graphed_fb_gives_the_same_training_step():
+    """F/B of every (stage, micro-batch, tape capture) as CUDA graphs
+    (CudaBackend(graph_fb=True)): the same kernels replayed, so the same
+    losses, factors and updated weights as the eager run, bit for bit."""
+    from paper_2211_14133_b200.engine import PipeFisherTrainer
+    runs = []
+    for gfb in (False, True):
+        cfg = S.PipelineConfig(stages=1, micro_batches=2, micro_batch_size=4, seq_len=64, layers_per_stage=2)
+        t = PipeFisherTrainer(cfg, small(), kfac=True, refresh=2, damping=0.1, lr=1e-2, seed=3, graph_fb=gfb)
+        losses = [t.run_cycle().loss for _ in range(3)]
+        torch.cuda.synchronize()
+        ks = t.backend.kstate[0]
+        runs.append((losses, {k: v.clone() for k, v in ks.factor.items()},
+                     [p.detach().clone() for p in t.backend.stages[0].parameters()]))
+        if gfb:
+            assert len(t.backend.graphed) == 4  # 2 micro-batches x (tape capture on / off)
+    (l0, f0, w0), (l1, f1, w1) = runs
+    assert l0 == l1
+    for k in f0:
+        assert torch.equal(f0[k], f1[k]), k
+    for a, b in zip(w0, w1):
+        assert torch.equal(a, b)

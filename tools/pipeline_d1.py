@@ -24,7 +24,8 @@ def main():
                            recompute=os.environ.get("PF_RECOMPUTE") == "1")
     out = {}
     for kfac in (True, False):
-        t = PipeFisherTrainer(cfg, bert, kfac=kfac, refresh=2, seed=11)
+        t = PipeFisherTrainer(cfg, bert, kfac=kfac, refresh=2, seed=11,
+                              graph_fb=os.environ.get("PF_GRAPH_FB") == "1")
         t.run_cycle()
         walls, steps = [], []
         for _ in range(3):
