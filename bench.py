@@ -550,6 +550,8 @@ def run_gpu_arm(args, rank, world, local_rank):
             prof["syrk"] = json.load(f).get("dram_bytes_per_launch")
         with open(os.path.join(ROOT, "profiles", "digit_gemm_traffic.json")) as f:
             prof["digit"] = json.load(f).get("dram_bytes_per_launch")
+        with open(os.path.join(ROOT, "profiles", "inversion_traffic.json")) as f:
+            prof["inversion"] = json.load(f).get("dram_bytes_per_call")
     except Exception:
         pass
     # Every phase is timed ALONE (graph-prefix replays, a few ms each), so its
@@ -565,7 +567,8 @@ def run_gpu_arm(args, rank, world, local_rank):
     roof = {"kernel": "damped inversion phase (12 factors: 2 x 4096 + 10 x 1024; leaves + digit GEMMs + "
                       "slicing, one CUDA graph) -- the dominant phase",
             "bound": "tensor", "achieved": inv_rate, "peak": digit_peak, "unit": "TFLOP/s (fp32-equivalent)",
-            "frac": inv_rate / digit_peak, "traffic": None,
+            "frac": inv_rate / digit_peak, "traffic": prof.get("inversion"),
+            "traffic_note": "per call, all 516 kernels, ncu with caches flushed per kernel (profiles/inversion_traffic.json); algorithmic ~0.56 GB",
             "algorithmic": "d^3 per factor (POTRF d^3/3 + TRTRI d^3/3 + LAUUM d^3/3): 148.0 GFLOP",
             "share_of_step": inv_ms / ms if ms > 0 else None,
             "peak_source": "measured int8 dense burst (cuBLASLt, profiles/int8_peak.json) / 10 digit products"}
