@@ -164,6 +164,40 @@ __device__ __forceinline__ void umma_i8(uint32_t d_tmem, uint64_t a_desc, uint64
         : "memory");
 }
 
+// The 10 digit products of one 32-byte k-step (kind::i8, s_a + s_b <= 3)
+// into the four weight accumulators t[g] (g = s_a + s_b), in ONE asm block:
+// as separate statements each MMA was wrapped by ptxas in its own
+// register -> uniform-register waterfall loop (~70 cycles per MMA, more than
+// a 128 x 32 x 32 MMA takes on the tensor core).  start_mask bit g: the
+// accumulator g already holds a partial sum (else its first product
+// overwrites it).
+__device__ __forceinline__ void umma_i8_digits(uint32_t t0, uint32_t t1, uint32_t t2, uint32_t t3,
+                                               const uint64_t (&a)[4], const uint64_t (&b)[4], uint32_t idesc,
+                                               uint32_t start_mask) {
+    asm volatile(
+        "{\n\t.reg .pred q0, q1, q2, q3, qt;\n\t"
+        ".reg .b32 m;\n\t"
+        "setp.eq.u32 qt, 0, 0;\n\t"
+        "and.b32 m, %13, 1;\n\tsetp.ne.b32 q0, m, 0;\n\t"
+        "and.b32 m, %13, 2;\n\tsetp.ne.b32 q1, m, 0;\n\t"
+        "and.b32 m, %13, 4;\n\tsetp.ne.b32 q2, m, 0;\n\t"
+        "and.b32 m, %13, 8;\n\tsetp.ne.b32 q3, m, 0;\n\t"
+        "tcgen05.mma.cta_group::1.kind::i8 [%0], %4, %8, %12, q0;\n\t"
+        "tcgen05.mma.cta_group::1.kind::i8 [%1], %4, %9, %12, q1;\n\t"
+        "tcgen05.mma.cta_group::1.kind::i8 [%1], %5, %8, %12, qt;\n\t"
+        "tcgen05.mma.cta_group::1.kind::i8 [%2], %4, %10, %12, q2;\n\t"
+        "tcgen05.mma.cta_group::1.kind::i8 [%2], %5, %9, %12, qt;\n\t"
+        "tcgen05.mma.cta_group::1.kind::i8 [%2], %6, %8, %12, qt;\n\t"
+        "tcgen05.mma.cta_group::1.kind::i8 [%3], %4, %11, %12, q3;\n\t"
+        "tcgen05.mma.cta_group::1.kind::i8 [%3], %5, %10, %12, qt;\n\t"
+        "tcgen05.mma.cta_group::1.kind::i8 [%3], %6, %9, %12, qt;\n\t"
+        "tcgen05.mma.cta_group::1.kind::i8 [%3], %7, %8, %12, qt;\n\t"
+        "}" ::"r"(t0),
+        "r"(t1), "r"(t2), "r"(t3), "l"(a[0]), "l"(a[1]), "l"(a[2]), "l"(a[3]), "l"(b[0]), "l"(b[1]), "l"(b[2]),
+        "l"(b[3]), "r"(idesc), "r"(start_mask)
+        : "memory");
+}
+
 // Arrive on `bar` once every previously issued tcgen05.mma of this thread
 // has completed (implies tcgen05.fence::before_thread_sync).
 __device__ __forceinline__ void umma_commit(uint64_t* bar) {

@@ -547,17 +547,14 @@ __global__ void __launch_bounds__(GemmTraits<kFmt, kN>::kThreads, GemmTraits<kFm
             for (int ks = 0; ks < T::kKSteps; ++ks) {
                 const uint32_t off = ks * 32;  // 32 B per UMMA k-step
                 if constexpr (kFmt == kOZ8) {
+                    uint64_t da[kDigits], db[kDigits];
 #pragma unroll
-                    for (int g = 0; g < kDigits; ++g) {
-#pragma unroll
-                        for (int sa = 0; sa <= g; ++sa) {
-                            const int sb = g - sa;
-                            const uint64_t da = ptx::sw64_kmajor_desc(ptx::smem_u32(a_plane(s, sa)) + off);
-                            const uint64_t db = ptx::sw64_kmajor_desc(ptx::smem_u32(b_plane(s, sb)) + off);
-                            ptx::umma_i8(tmem + g * kN, da, db, T::kIdesc, (started >> g) & 1u);
-                            started |= 1u << g;
-                        }
+                    for (int q = 0; q < kDigits; ++q) {
+                        da[q] = ptx::sw64_kmajor_desc(ptx::smem_u32(a_plane(s, q)) + off);
+                        db[q] = ptx::sw64_kmajor_desc(ptx::smem_u32(b_plane(s, q)) + off);
                     }
+                    ptx::umma_i8_digits(tmem, tmem + kN, tmem + 2 * kN, tmem + 3 * kN, da, db, T::kIdesc, started);
+                    started = 0xFu;
                 } else if (P.mn_major) {
                     // 16 K rows per UMMA = two 8-row groups of 1024 B
                     const uint32_t moff = ks * 2048;
@@ -779,17 +776,15 @@ __global__ void __launch_bounds__(kPersistThreads, 1)
 #pragma unroll
                     for (int ks = 0; ks < T::kKSteps; ++ks) {
                         const uint32_t off = ks * 32;
+                        uint64_t da[kDigits], db[kDigits];
 #pragma unroll
-                        for (int g = 0; g < kDigits; ++g) {
-#pragma unroll
-                            for (int sa = 0; sa <= g; ++sa) {
-                                const int sb = g - sa;
-                                const uint64_t da = ptx::sw64_kmajor_desc(ptx::smem_u32(a_plane(s, sa)) + off);
-                                const uint64_t db = ptx::sw64_kmajor_desc(ptx::smem_u32(b_plane(s, sb)) + off);
-                                ptx::umma_i8(tmem + g * kTile, da, db, T::kIdesc, (started >> g) & 1u);
-                                started |= 1u << g;
-                            }
+                        for (int q = 0; q < kDigits; ++q) {
+                            da[q] = ptx::sw64_kmajor_desc(ptx::smem_u32(a_plane(s, q)) + off);
+                            db[q] = ptx::sw64_kmajor_desc(ptx::smem_u32(b_plane(s, q)) + off);
                         }
+                        ptx::umma_i8_digits(tmem, tmem + kTile, tmem + 2 * kTile, tmem + 3 * kTile, da, db, T::kIdesc,
+                                            started);
+                        started = 0xFu;
                     }
                     ptx::umma_commit(&empty[s]);
                     if (++s == kStages) {
