@@ -240,7 +240,29 @@ class LayerStep:
         K.precondition_update_sliced(items)
 
 
-def self_check(torch, st, step_a, step_b):
+def sync_factors(torch, dist, factors, tril):
+    """SyncCurvature of the N > 1 layer step: the replica average of the
+    factors.  The SYRK writes lower tiles only, so the packed lower triangles
+    of all factors travel in ONE all-reduce (sum d(d+1)/2 floats: 88 MB for the
+    BERT-Large layer instead of 168 MB of full squares in 12 calls)."""
+    packed = torch.cat([f.view(-1).index_select(0, i) for f, i in zip(factors, tril)])
+    dist.all_reduce(packed, op=dist.ReduceOp.AVG)
+    off = 0
+    for f, i in zip(factors, tril):
+        f.view(-1).index_copy_(0, i, packed[off:off + i.numel()])
+        off += i.numel()
+
+
+def share_inverses(dist, digits, world):
+    """Inversion parallelism: factor i was inverted on rank i % world; only its
+    digit form travels (all the preconditioner reads), as asynchronous
+    broadcasts waited together."""
+    works = [dist.broadcast(dg, src=i % world, async_op=True) for i, dg in enumerate(digits)]
+    for w in works:
+        w.wait()
+
+
+def self_check(torch, st, step_a, step_b, owned=None):
     """The bench checks its OWN step (outside the timed region), in fp64 on the
     device: the damped-inverse residual max|(A + lambda I) X - I| of every
     factor the step inverted (reference norm, proj/tests/test_kfac.cpp:155;
@@ -251,11 +273,13 @@ def self_check(torch, st, step_a, step_b):
     torch.cuda.synchronize()
     f64 = torch.float64
     damped, resid = [], {}
-    for f, x in zip(st.factors, st.inv):
+    for i, (f, x) in enumerate(zip(st.factors, st.inv)):
         d = f.shape[0]
         a = f.to(f64)
         a = torch.tril(a) + torch.tril(a, -1).T + DAMPING * torch.eye(d, device=f.device, dtype=f64)
         damped.append(a)
+        if owned is not None and i not in owned:
+            continue  # inverted on another rank (only its digit form travels)
         r = (a @ x.to(f64) - torch.eye(d, device=f.device, dtype=f64)).abs().max().item()
         resid[str(d)] = max(resid.get(str(d), 0.0), r)
     w0 = [w.clone() for w in st.weights]
@@ -270,7 +294,7 @@ def self_check(torch, st, step_a, step_b):
         rel = max(rel, ((got - want).norm() / want.norm()).item())
     return {"inverse_residual_max": resid, "inverse_residual_bound": 1e-5,
             "update_rel_fro_max": rel, "update_rel_fro_bound": 1e-3,
-            "ok": max(resid.values()) <= 1e-5 and rel <= 1e-3,
+            "ok": max(resid.values(), default=0.0) <= 1e-5 and rel <= 1e-3,
             "how": "fp64 on the device, after the timed region, on the step's own factors / inverses / weights"}
 
 
@@ -288,11 +312,13 @@ def run_gpu_arm(args, rank, world, local_rank):
     st = LayerStep(torch, K, seed=1234 + rank)
     stream = torch.cuda.current_stream()
 
+    tril = None
+    if world > 1:
+        from paper_2211_14133_b200.engine import _tril_index
+        tril = [_tril_index(f.shape[0], f.device) for f in st.factors]
+
     def exchange():
-        # SyncCurvature: average factors over data-parallel replicas (NCCL),
-        # then inversion parallelism: factor i inverted on rank i % world.
-        for f in st.factors:
-            dist.all_reduce(f, op=dist.ReduceOp.AVG)
+        sync_factors(torch, dist, st.factors, tril)
 
     def step(ev=None):
         step_a(ev)
@@ -304,11 +330,12 @@ def run_gpu_arm(args, rank, world, local_rank):
         if ev: ev[1].record(stream)
         if world > 1:
             exchange()
+            # inversion parallelism: factor i inverted on rank i % world; only
+            # the digit form travels (all the preconditioner reads), as
+            # asynchronous broadcasts waited together
             mine = [i for i in range(len(st.factors)) if i % world == rank]
             st.invert(mine)
-            for i in range(len(st.factors)):
-                dist.broadcast(st.inv[i], src=i % world)
-                dist.broadcast(st.digits[i], src=i % world)
+            share_inverses(dist, st.digits, world)
         else:
             st.invert()
         if ev: ev[2].record(stream)
@@ -535,7 +562,8 @@ def run_gpu_arm(args, rank, world, local_rank):
         e2e_ms = float(t.item())
     e2e_value = job_flops / (e2e_ms * 1e-3) / 1e12
 
-    check = self_check(torch, st, step_a, step_b)
+    check = self_check(torch, st, step_a, step_b,
+                       owned=None if world == 1 else {i for i in range(len(st.factors)) if i % world == rank})
     pipeline = None if args.no_pipeline else pipeline_section(args, rank, world, local_rank, dist)
 
     if rank != 0:
