@@ -437,7 +437,8 @@ void launch_gemms_n(const std::vector<GemmSpec>& specs_in, cudaStream_t stream) 
             // long-K launches with more tiles than SMs: persistent CTAs
             int kmin = 1 << 30;
             for (int q = 0; q < probs; ++q) kmin = std::min(kmin, batch.probs[q].k);
-            if (gemm_persist_enabled() && kmin > 512 && tiles > sm_count()) {
+            static const int pk = [] { const char* e = std::getenv("PF_PERSIST_KMIN"); return e ? std::atoi(e) : 512; }();
+            if (gemm_persist_enabled() && kmin > pk && tiles > sm_count()) {
                 static std::once_flag once;
                 std::call_once(once, [] {
                     check(cudaFuncSetAttribute(umma_gemm_persist_kernel<kSplit>, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -481,8 +482,13 @@ int pick_tile_n(const std::vector<GemmSpec>& specs) {
         tiles += static_cast<long>((g.rows + kTile - 1) / kTile) * ((g.cols + kTile - 1) / kTile);
     }
     const int sms = sm_count();
-    if (tiles * 4 <= sms) return 32;
-    if (tiles * 2 <= sms) return 64;
+    // a launch of at most sms / f32 (sms / f64) 128-wide tiles splits them 4 (2)
+    // ways; re-tuned in round 2 with the faster leaf (layer inversion 2.49 ->
+    // 2.44 ms against f32 = 4, f64 = 2); PF_NSPLIT32 / PF_NSPLIT64 override
+    static const int f32 = [] { const char* e = std::getenv("PF_NSPLIT32"); return e ? std::atoi(e) : 8; }();
+    static const int f64 = [] { const char* e = std::getenv("PF_NSPLIT64"); return e ? std::atoi(e) : 4; }();
+    if (tiles * f32 <= sms) return 32;
+    if (tiles * f64 <= sms) return 64;
     return kTile;
 }
 
@@ -698,7 +704,8 @@ struct Emitter {
 };
 
 // A group with a SHORTER chain than the lead (smaller d) of a right-looking
-// call starts when the lead's factorisation reaches panel nb_lead - 2 nb_g:
+// call starts when the lead's factorisation reaches panel nb_lead - 1.5 nb_g
+// (PF_DELAY_MUL, re-tuned in round 2; was 2 nb_g):
 // started together it takes SMs from the lead's launch-latency-bound chain for
 // its whole length; started late it still finishes before the lead's TRTRI /
 // LAUUM tail (2x4096 + 10x1024, start panel of the 1024 groups: 0 -> 2.79 ms,
@@ -1772,7 +1779,11 @@ int pf_damped_inverse_batched(const pf_inverse_problem* problems, int count, voi
             run_forked(groups.size(), st, [&](std::size_t g, cudaStream_t s) {
                 const int d_g = groups[g].front()->d;
                 if (g > 0 && d_g < lead_d && g_lead_panels > 0) {
-                    const int start = g_lead_panels - 2 * ((d_g + kLeaf - 1) / kLeaf);
+                    static const double mul = [] {
+                        const char* e = std::getenv("PF_DELAY_MUL");
+                        return e ? std::atof(e) : 1.5;  // round 2 re-tune (2.0: 2.437 ms, 1.5: 2.415)
+                    }();
+                    const int start = g_lead_panels - static_cast<int>(mul * ((d_g + kLeaf - 1) / kLeaf));
                     if (start > 0)
                         check(cudaStreamWaitEvent(s, pool_event(kMarkGroup, start), 0), "lead mark wait");
                 }
