@@ -691,7 +691,8 @@ def pipeline_section(args, rank, world, local_rank, dist):
                                      "cost_table": {k: getattr(t.costs, k) for k in
                                                     ("t_f", "t_b", "t_curv", "t_inv", "t_prec")},
                                      "source": "CUDA events on this GPU, median of 3, max over ranks"}
-        t.run_cycle()  # warm-up (allocations, cuBLAS heuristics)
+        for _ in range(2):  # warm-up (allocations, cuBLAS heuristics, F/B and inversion graph captures)
+            t.run_cycle()
         if dist: dist.barrier()
         res = [t.run_cycle(record=(i == 1)) for i in range(2)]
         step = statistics.mean(r.step_ms for r in res)

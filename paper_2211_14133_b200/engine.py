@@ -12,6 +12,8 @@ Per hosted stage and encoder layer the factor sets are:
 """
 from __future__ import annotations
 
+import os
+
 import math
 import time
 from dataclasses import dataclass
@@ -129,6 +131,7 @@ class CudaBackend:
         # cycle-end join with the K-FAC stream.
         self.graph_fb = bool(graph_fb) and not self.recompute_on
         self.graphed: Dict[Tuple[int, int, bool], object] = {}
+        self.inv_graphs: Dict[Tuple[int, ...], torch.cuda.CUDAGraph] = {}  # batched inversions (graph_fb)
         self.cur_step = 0  # set by the executor before each op (trace metadata)
 
     # ------------------------------------------------------------ timing helpers
@@ -306,7 +309,24 @@ class CudaBackend:
                     outs.append(o.fp32)
                     digs.append(o.digits)
             e0 = self._begin(self.kfac_stream)
-            K.damped_inverse_batched(mats, self.damping, outs, digs, check=False)
+            if self.graph_fb:
+                # a batched inversion is thousands of dependent launches: the
+                # first call with a set of buffers runs eagerly (library
+                # warm-up) and is then captured as a CUDA graph that every
+                # later call replays (24-layer batch: 47 -> ~27 ms, host-bound
+                # when issued eagerly)
+                key = tuple(t.data_ptr() for t in mats + outs + digs)
+                g = self.inv_graphs.get(key)
+                if g is not None:
+                    g.replay()
+                else:
+                    K.damped_inverse_batched(mats, self.damping, outs, digs, check=False)
+                    g = torch.cuda.CUDAGraph()
+                    with torch.cuda.graph(g, stream=self.kfac_stream):
+                        K.damped_inverse_batched(mats, self.damping, outs, digs, check=False)
+                    self.inv_graphs[key] = g
+            else:
+                K.damped_inverse_batched(mats, self.damping, outs, digs, check=False)
             st0, l0, f0 = items[0]
             self._end("INV", e0, self.kfac_stream, stage=st0, layer=l0, factor=f0, items=len(items))
             ev = torch.cuda.Event()
@@ -486,15 +506,21 @@ def measure_stage_times(backend: "CudaBackend", reps: int = 3) -> MeasuredTimes:
         for p in mod.parameters():
             p.grad = None
     curv, inv = [], []
-    for i in range(reps + 1):
+    for i in range(reps + 1):  # curvature first: no graph capture (synchronize, empty_cache) in between
         for f in (0, 1):
             pc = timed(lambda: backend.curvature_many([(stage, 0, f, micro)], None), backend.kfac_stream)
-            pi = timed(lambda: backend.invert_many([(stage, 0, f)], None), backend.kfac_stream)
             if i:
                 curv.append(pc)
+    for i in range(reps + 2):  # round 0 captures the inversion graphs (graph_fb), round 1 uploads them
+        for f in (0, 1):
+            pi = timed(lambda: backend.invert_many([(stage, 0, f)], None), backend.kfac_stream)
+            if i >= 2:
                 inv.append(pi)
     t_curv = median_ms(curv[0::2]), median_ms(curv[1::2])
     t_inv = median_ms(inv[0::2]), median_ms(inv[1::2])
+    if os.environ.get("PF_DEBUG_TIMES"):
+        print("measure_stage_times inv", [a.elapsed_time(b) for a, b in inv],
+              "curv", [a.elapsed_time(b) for a, b in curv], flush=True)
     prec = []
     for i in range(reps + 1):
         backend.forward(stage, micro, None if x is None else x.clone(), False, 0)

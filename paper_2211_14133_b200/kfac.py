@@ -79,11 +79,17 @@ class _Workspaces:
 
     def __init__(self):
         self._bufs: Dict[Tuple[int, str, int], torch.Tensor] = {}
+        # buffers replaced by a bigger one stay allocated: a CUDA graph
+        # captured while one was current still reads and writes it at every
+        # replay (freeing it crashed such a replay)
+        self._retired: List[torch.Tensor] = []
 
     def get(self, nbytes: int, device: torch.device, tag: str = "ws") -> torch.Tensor:
         key = (device.index or 0, tag, torch.cuda.current_stream(device).cuda_stream)
         buf = self._bufs.get(key)
         if buf is None or buf.numel() < nbytes:
+            if buf is not None:
+                self._retired.append(buf)
             buf = torch.empty(max(nbytes, 256), dtype=torch.uint8, device=device)
             self._bufs[key] = buf
         return buf

@@ -420,3 +420,41 @@ def test_syrk_token_major_grouped_accumulate_with_padded_rows(K):
     wb = 0.5 + 2.0 * (b.float().t() @ b.float())
     assert ((fa - wa).norm() / wa.norm()).item() < 1e-5
     assert ((fb - wb).norm() / wb.norm()).item() < 1e-5
+
+
+def test_graphs_captured_after_eager_calls_survive_workspace_growth(K):
+    """A batched inversion run eagerly and then captured as a CUDA graph on the
+    same stream, followed by a bigger batch that grows the workspace arena:
+    replaying the first graph must still find its workspace (the arena keeps
+    replaced buffers alive) and reproduce the eager result bit for bit."""
+    s = torch.cuda.Stream()
+
+    def mk(n, seed):
+        g = torch.Generator(device="cuda").manual_seed(seed)
+        mats = []
+        for d in [256] * n + [512]:
+            x = torch.randn((d, 1024), generator=g, device="cuda").to(torch.bfloat16).float()
+            mats.append(x @ x.T / 1024)
+        outs = [torch.empty_like(m) for m in mats]
+        digs = [torch.empty(K.slice_bytes(m.shape[0], m.shape[0]), dtype=torch.uint8, device="cuda") for m in mats]
+        return mats, outs, digs
+
+    sets = [mk(2, 1), mk(5, 2)]
+    graphs, eager = [], []
+    for mats, outs, digs in sets:
+        with torch.cuda.stream(s):
+            K.damped_inverse_batched(mats, 0.1, outs, digs, check=False)
+        torch.cuda.synchronize()
+        eager.append([o.clone() for o in outs])
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g, stream=s):
+            K.damped_inverse_batched(mats, 0.1, outs, digs, check=False)
+        graphs.append(g)
+    for (mats, outs, digs), g, want in zip(sets, graphs, eager):
+        for o in outs:
+            o.zero_()
+        with torch.cuda.stream(s):
+            g.replay()
+        torch.cuda.synchronize()
+        for o, w in zip(outs, want):
+            assert torch.equal(o, w)

@@ -27,13 +27,22 @@ def main():
         t = PipeFisherTrainer(cfg, bert, kfac=kfac, refresh=2, seed=11,
                               graph_fb=os.environ.get("PF_GRAPH_FB") == "1")
         t.run_cycle()
+        t.run_cycle()  # the second call of a batched inversion captures its graph
         walls, steps = [], []
         for _ in range(3):
             w0 = time.perf_counter()
             r = t.run_cycle()
             walls.append((time.perf_counter() - w0) * 1e3 / t.refresh)
             steps.append(r.step_ms)
+        r = t.run_cycle(record=True)
+        kinds = {}
+        for kind, a, b, m in getattr(t, "last_trace", []):
+            kinds.setdefault(kind, [0, 0.0])
+            kinds[kind][0] += 1
+            kinds[kind][1] += b - a
         out["kfac" if kfac else "plain"] = {"step_ms": sum(steps) / 3, "host_wall_ms_per_step": sum(walls) / 3,
+                                            "op_ms_per_cycle": {k: {"ops": v[0], "ms": round(v[1], 3)} for k, v in kinds.items()},
+                                            "cycle_ms": r.step_ms * t.refresh,
                                             "cupti": kernel_activity(t)}
         del t
         torch.cuda.empty_cache()
