@@ -16,17 +16,17 @@ grep '^{' $OUT/log.txt | tail -1 > $OUT/bench.json
 run timeout 300 ncu --profile-from-start off --metrics gpu__time_duration.sum --clock-control none --csv \
     --log-file $OUT/launches.csv python tools/prof_phase.py step 2
 cap() {  # name phase kernel-regex skip
-  run timeout 600 ncu --profile-from-start off --set full --clock-control none --import-source on --kernel-name-base demangled \
+  run timeout 600 ncu --profile-from-start off --set full --clock-control none --import-source on --kernel-name-base mangled \
       -k "regex:$3" -s ${4:-0} -c 1 -o $OUT/$1 python tools/prof_phase.py $2 1
 }
-cap syrk curvature 'umma_gemm_kernel<1'
-cap prec precondition 'umma_gemm_persist'
-cap gemm32 inversion 'umma_gemm_kernel<3, 32' 20
-cap gemm64 inversion 'umma_gemm_kernel<3, 64' 10
-cap gemm128 inversion 'umma_gemm_kernel<3, 128' 10
+cap syrk curvature 'umma_gemm_kernelILi1E'
+cap prec precondition 'umma_gemm_persist_kernelILb0'
+cap gemm32 inversion 'umma_gemm_kernelILi3ELi32E' 20
+cap gemm64 inversion 'umma_gemm_kernelILi3ELi64E' 10
+cap gemm128 inversion 'umma_gemm_kernelILi3ELi128ELb0' 10
 cap leaf inversion 'leaf_chol' 10
 cap slice_short inversion 'slice_short' 20
 cap slice_long inversion 'slice_long'
 cap damp inversion 'damp_kernel'
-cap lauum inversion 'umma_gemm_persist_kernel<true' 
+cap lauum inversion 'umma_gemm_persist_kernelILb1'
 echo finished >> $OUT/log.txt
