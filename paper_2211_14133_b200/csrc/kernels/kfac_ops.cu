@@ -88,16 +88,24 @@ struct ScopedPrio {
     ~ScopedPrio() { g_launch_prio = saved; }
 };
 
+// cluster_x > 1: thread-block clusters of cluster_x CTAs along x
 template <typename... KArgs, typename... Args>
-void launch(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t st,
-            Args&&... args) {
+void launch_cluster(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t st,
+                    int cluster_x, Args&&... args) {
     cudaLaunchConfig_t cfg{};
     cfg.gridDim = grid;
     cfg.blockDim = block;
     cfg.dynamicSmemBytes = smem;
     cfg.stream = st;
-    cudaLaunchAttribute attr[2];
+    cudaLaunchAttribute attr[3];
     int na = 0;
+    if (cluster_x > 1) {
+        attr[na].id = cudaLaunchAttributeClusterDimension;
+        attr[na].val.clusterDim.x = static_cast<unsigned>(cluster_x);
+        attr[na].val.clusterDim.y = 1;
+        attr[na].val.clusterDim.z = 1;
+        ++na;
+    }
     if (pdl_enabled()) {
         attr[na].id = cudaLaunchAttributeProgrammaticStreamSerialization;
         attr[na].val.programmaticStreamSerializationAllowed = 1;
@@ -111,6 +119,12 @@ void launch(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaSt
     cfg.attrs = attr;
     cfg.numAttrs = na;
     check(cudaLaunchKernelEx(&cfg, kernel, std::forward<Args>(args)...), "cudaLaunchKernelEx");
+}
+
+template <typename... KArgs, typename... Args>
+void launch(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t st,
+            Args&&... args) {
+    launch_cluster(kernel, grid, block, smem, st, 1, std::forward<Args>(args)...);
 }
 
 inline int round_up(int x, int m) { return (x + m - 1) / m * m; }
@@ -393,6 +407,40 @@ int ticket_slot(cudaStream_t stream) {
     return kEagerSlots + static_cast<int>(c);
 }
 
+// Split-K factor of a bf16 (SYRK) launch.  A CTA of the SYRK streams 32 KB
+// of operands per 64-wide k-block through its SM, and one SM pulls ~100-120
+// GB/s from L2 (measured: a lone 128x128 tile runs ~0.33 us per k-block, 4x
+// its MMA time) -- so a launch of few tiles (a d = 1024 factor has 36) is
+// bound by the bandwidth of the few SMs it occupies.  Splitting every tile's
+// k-blocks over a cluster of 2 or 4 CTAs puts more SMs on it; the partial
+// tiles are summed over DSMEM in a fixed order (umma_gemm.cuh
+// split_k_epilogue), so results do not depend on timing.
+//   4 slices: only while all CTAs get an SM of their own (tiles x 4 <=
+//             0.8 SMs; a cluster must fit inside one GPC, and 4-CTA clusters
+//             beyond that double up on SMs);
+//   2 slices: while tiles x 2 <= 2 CTAs per SM (the kernel's occupancy);
+// each slice keeps >= PF_KSPLIT_MINKB (default 8) k-blocks.  8-CTA clusters
+// measured slower than 4 everywhere (ubench_syrk_splitk.txt).  PF_KSPLIT=n
+// forces n (1 = off) for measurements.
+int bf16_k_split(const GemmBatch& b, int tiles) {
+    static const int force = [] { const char* e = std::getenv("PF_KSPLIT"); return e ? std::atoi(e) : 0; }();
+    static const int min_kb = [] { const char* e = std::getenv("PF_KSPLIT_MINKB"); return e ? std::atoi(e) : 8; }();
+    int kb = 1 << 30;
+    for (int q = 0; q < b.n_probs; ++q) {
+        if (b.probs[q].k_mode != K_FULL) return 1;
+        kb = std::min(kb, (b.probs[q].k + 63) / 64);
+    }
+    if (force >= 1) {
+        int f = 1;
+        while (f * 2 <= std::min(force, 8)) f *= 2;
+        return f;
+    }
+    const long sms = sm_count();
+    if (static_cast<long>(tiles) * 4 * 5 <= sms * 4 && kb / 4 >= min_kb) return 4;
+    if (static_cast<long>(tiles) * 2 <= 2 * sms && kb / 2 >= min_kb) return 2;
+    return 1;
+}
+
 template <int kFmt, int kN, bool kSplit = false>
 void launch_gemms_n(const std::vector<GemmSpec>& specs_in, cudaStream_t stream) {
     using T = GemmTraits<kFmt, kN>;
@@ -449,6 +497,15 @@ void launch_gemms_n(const std::vector<GemmSpec>& specs_in, cudaStream_t stream) 
                 launch(umma_gemm_persist_kernel<kSplit>, dim3(std::min(tiles, sm_count())), dim3(kPersistThreads),
                        T::kSmemBytes, stream, batch, slot);
                 after_launch("umma_gemm_persist_kernel");
+                continue;
+            }
+        }
+        if constexpr (kFmt == kBF16) {
+            batch.k_split = bf16_k_split(batch, tiles);
+            if (batch.k_split > 1) {
+                launch_cluster(kernel, dim3(tiles * batch.k_split), dim3(T::kThreads), T::kSmemBytes, stream,
+                               batch.k_split, batch);
+                after_launch("umma_gemm_kernel");
                 continue;
             }
         }

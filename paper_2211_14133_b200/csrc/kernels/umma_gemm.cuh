@@ -125,6 +125,8 @@ struct GemmBatch {
     int n_probs;
     int total_tiles;
     int interleave;  // all problems share tile count and k-mode: tile rank major, problem minor
+    int k_split;     // kBF16: >= 2 -> clusters of k_split CTAs per tile, each one k_split-th of
+                     // the k-blocks; the partial tiles are summed over DSMEM in cluster-rank order
 };
 
 // kN: tile width (columns of C, rows of B).  128 everywhere except short
@@ -222,6 +224,83 @@ __device__ __forceinline__ EpiRow epi_row(const GemmDesc& P, int tm, int tn, int
     return e;
 }
 
+// beta * C and the stores of one 16-column chunk of tile row r (global row)
+template <int kN>
+__device__ __forceinline__ void finish_chunk(const GemmDesc& P, int tm, int tn, int r, int chunk, float (&out)[16],
+                                             const float* crow) {
+    const uint32_t f = P.flags;
+    const bool row_ok = r < P.rows;
+    const bool mirror = (f & EPI_MIRROR) && tm != tn;
+    const int c0 = tn * kN + chunk * 16;
+    if (!row_ok || c0 >= P.cols) return;
+    const bool full_chunk = c0 + 16 <= P.cols;
+    if (P.beta != 0.0f) {
+        float cv[16];
+        if (crow && full_chunk) {  // C row prefetched into shared memory
+            const float4* src = reinterpret_cast<const float4*>(crow + chunk * 16);
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+                const float4 t = src[q];
+                cv[4 * q] = t.x;
+                cv[4 * q + 1] = t.y;
+                cv[4 * q + 2] = t.z;
+                cv[4 * q + 3] = t.w;
+            }
+        } else if ((f & EPI_VEC4) && full_chunk && !(f & EPI_TRANSPOSE)) {
+            const float4* src = reinterpret_cast<const float4*>(P.c + static_cast<size_t>(r) * P.ldc + c0);
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+                const float4 t = __ldcg(src + q);
+                cv[4 * q] = t.x;
+                cv[4 * q + 1] = t.y;
+                cv[4 * q + 2] = t.z;
+                cv[4 * q + 3] = t.w;
+            }
+        } else {
+#pragma unroll
+            for (int j = 0; j < 16; ++j) {
+                const int c = c0 + j;
+                const size_t idx = (f & EPI_TRANSPOSE) ? static_cast<size_t>(c) * P.ldc + r
+                                                       : static_cast<size_t>(r) * P.ldc + c;
+                cv[j] = c < P.cols ? __ldcg(P.c + idx) : 0.0f;
+            }
+        }
+#pragma unroll
+        for (int j = 0; j < 16; ++j) out[j] = fmaf(P.beta, cv[j], out[j]);
+    }
+#ifdef PF_PROBE_NOSTORE
+    if (P.beta != 0.0f && P.rows <= kTile && P.cols <= kTile) {
+        if (out[0] == 12345.678f) P.c[0] = out[1];  // keep the values live
+        return;
+    }
+#endif
+    if ((f & EPI_VEC4) && full_chunk && !(f & EPI_TRANSPOSE)) {
+        float4* dst = reinterpret_cast<float4*>(P.c + static_cast<size_t>(r) * P.ldc + c0);
+#pragma unroll
+        for (int q = 0; q < 4; ++q)
+            dst[q] = make_float4(out[4 * q], out[4 * q + 1], out[4 * q + 2], out[4 * q + 3]);
+    } else if (f & EPI_TRANSPOSE) {
+        // lanes hold consecutive rows -> each transposed column store is coalesced
+#pragma unroll
+        for (int j = 0; j < 16; ++j)
+            if (c0 + j < P.cols) P.c[static_cast<size_t>(c0 + j) * P.ldc + r] = out[j];
+    } else {
+#pragma unroll
+        for (int j = 0; j < 16; ++j)
+            if (c0 + j < P.cols) P.c[static_cast<size_t>(r) * P.ldc + c0 + j] = out[j];
+    }
+    if (mirror) {
+#pragma unroll
+        for (int j = 0; j < 16; ++j)
+            if (c0 + j < P.cols) P.c[static_cast<size_t>(c0 + j) * P.ldc + r] = out[j];
+    }
+    if (f & EPI_ALSO_T) {
+#pragma unroll
+        for (int j = 0; j < 16; ++j)
+            if (c0 + j < P.cols) P.c_t[static_cast<size_t>(c0 + j) * P.ldc_t + r] = out[j];
+    }
+}
+
 // col_scale: kOZ8 -> 2^e_b per tile column, kBF16 -> unused.
 // kSplit: the EPI_DIAG_SPLIT variant (a separate instantiation: its extra
 // loads and registers stay out of every other digit GEMM)
@@ -231,82 +310,11 @@ __device__ __forceinline__ void epilogue_chunks(const GemmDesc& P, int tm, int t
                                                 bool have_acc, const EpiRow& er, const float* crow = nullptr) {
     const bool row_ok = r < P.rows;
     const uint32_t f = P.flags;
-    const bool mirror = (f & EPI_MIRROR) && tm != tn;
     const float row_scale = er.row_scale;
     const bool exact_diag = (f & EPI_EXACT_DIAG) && row_ok;  // diag_chunk below: global r == c
     const float diag_exact = er.diag_exact;
     PF_ESTAMP(0);
-    // beta * C and the stores of one 16-column chunk
-    auto finish = [&](float (&out)[16], int chunk) {
-        const int c0 = tn * kN + chunk * 16;
-        if (!row_ok || c0 >= P.cols) return;
-        const bool full_chunk = c0 + 16 <= P.cols;
-        if (P.beta != 0.0f) {
-            float cv[16];
-            if (crow && full_chunk) {  // C row prefetched into shared memory
-                const float4* src = reinterpret_cast<const float4*>(crow + chunk * 16);
-#pragma unroll
-                for (int q = 0; q < 4; ++q) {
-                    const float4 t = src[q];
-                    cv[4 * q] = t.x;
-                    cv[4 * q + 1] = t.y;
-                    cv[4 * q + 2] = t.z;
-                    cv[4 * q + 3] = t.w;
-                }
-            } else if ((f & EPI_VEC4) && full_chunk && !(f & EPI_TRANSPOSE)) {
-                const float4* src = reinterpret_cast<const float4*>(P.c + static_cast<size_t>(r) * P.ldc + c0);
-#pragma unroll
-                for (int q = 0; q < 4; ++q) {
-                    const float4 t = __ldcg(src + q);
-                    cv[4 * q] = t.x;
-                    cv[4 * q + 1] = t.y;
-                    cv[4 * q + 2] = t.z;
-                    cv[4 * q + 3] = t.w;
-                }
-            } else {
-#pragma unroll
-                for (int j = 0; j < 16; ++j) {
-                    const int c = c0 + j;
-                    const size_t idx = (f & EPI_TRANSPOSE) ? static_cast<size_t>(c) * P.ldc + r
-                                                           : static_cast<size_t>(r) * P.ldc + c;
-                    cv[j] = c < P.cols ? __ldcg(P.c + idx) : 0.0f;
-                }
-            }
-#pragma unroll
-            for (int j = 0; j < 16; ++j) out[j] = fmaf(P.beta, cv[j], out[j]);
-        }
-#ifdef PF_PROBE_NOSTORE
-        if (P.beta != 0.0f && P.rows <= kTile && P.cols <= kTile) {
-            if (out[0] == 12345.678f) P.c[0] = out[1];  // keep the values live
-            return;
-        }
-#endif
-        if ((f & EPI_VEC4) && full_chunk && !(f & EPI_TRANSPOSE)) {
-            float4* dst = reinterpret_cast<float4*>(P.c + static_cast<size_t>(r) * P.ldc + c0);
-#pragma unroll
-            for (int q = 0; q < 4; ++q)
-                dst[q] = make_float4(out[4 * q], out[4 * q + 1], out[4 * q + 2], out[4 * q + 3]);
-        } else if (f & EPI_TRANSPOSE) {
-            // lanes hold consecutive rows -> each transposed column store is coalesced
-#pragma unroll
-            for (int j = 0; j < 16; ++j)
-                if (c0 + j < P.cols) P.c[static_cast<size_t>(c0 + j) * P.ldc + r] = out[j];
-        } else {
-#pragma unroll
-            for (int j = 0; j < 16; ++j)
-                if (c0 + j < P.cols) P.c[static_cast<size_t>(r) * P.ldc + c0 + j] = out[j];
-        }
-        if (mirror) {
-#pragma unroll
-            for (int j = 0; j < 16; ++j)
-                if (c0 + j < P.cols) P.c[static_cast<size_t>(c0 + j) * P.ldc + r] = out[j];
-        }
-        if (f & EPI_ALSO_T) {
-#pragma unroll
-            for (int j = 0; j < 16; ++j)
-                if (c0 + j < P.cols) P.c_t[static_cast<size_t>(c0 + j) * P.ldc_t + r] = out[j];
-        }
-    };
+    auto finish = [&](float (&out)[16], int chunk) { finish_chunk<kN>(P, tm, tn, r, chunk, out, crow); };
     // the diagonal of a same-operand product: exact norm of the represented row
     auto diag_fix = [&](float (&out)[16], int chunk) {
         const int c0 = tn * kN + chunk * 16;
@@ -422,6 +430,67 @@ __device__ __forceinline__ void epilogue_chunks(const GemmDesc& P, int tm, int t
     }
 }
 
+// kBF16 split-K epilogue (GemmBatch::k_split): every CTA of the cluster parks
+// its partial tile in its idle stage buffers, then CTA `kslice` sums rows
+// [kslice R, (kslice+1) R) over the cluster's CTAs in rank order (the same
+// sum whichever CTA finished first) and runs the epilogue on them.
+template <int kN, int kThreads>
+__device__ __forceinline__ void split_k_epilogue(const GemmDesc& P, int tm, int tn, uint8_t* smem, uint32_t tmem,
+                                                 int ks, int kslice, bool have_acc) {
+    const int warp = threadIdx.x >> 5;
+    const uint32_t lane = threadIdx.x & 31;
+    constexpr int kRS = kN + 4;  // row stride (floats): float4 accesses by row-strided lanes conflict-free
+    float* red = reinterpret_cast<float*>(smem);
+    const int row = warp * 32 + static_cast<int>(lane);
+#pragma unroll 1
+    for (int chunk = 0; chunk < kN / 16; ++chunk) {
+        __syncwarp();
+        float v[16];
+        if (have_acc) {
+            ptx::tmem_ld16(tmem + (static_cast<uint32_t>(warp * 32) << 16) + chunk * 16, v);
+        } else {
+#pragma unroll
+            for (int j = 0; j < 16; ++j) v[j] = 0.0f;
+        }
+        float4* dst = reinterpret_cast<float4*>(red + row * kRS + chunk * 16);
+#pragma unroll
+        for (int q = 0; q < 4; ++q) dst[q] = make_float4(v[4 * q], v[4 * q + 1], v[4 * q + 2], v[4 * q + 3]);
+    }
+    ptx::tc_fence_before();
+    ptx::cluster_sync();
+    const int rows = kTile / ks;
+    const uint32_t red_u32 = ptx::smem_u32(red);
+#pragma unroll 1
+    for (int w = threadIdx.x; w < rows * (kN / 16); w += kThreads) {
+        const int rr = kslice * rows + w % rows, chunk = w / rows;  // lanes: consecutive rows
+        const uint32_t off = static_cast<uint32_t>((rr * kRS + chunk * 16) * 4);
+        float out[16];
+#pragma unroll 1
+        for (int q = 0; q < ks; ++q) {
+            const uint32_t a = ptx::mapa(red_u32 + off, static_cast<uint32_t>(q));
+#pragma unroll
+            for (int h = 0; h < 4; ++h) {
+                const float4 t = ptx::ld_dsmem4(a + 16 * h);
+                if (q == 0) {
+                    out[4 * h] = t.x;
+                    out[4 * h + 1] = t.y;
+                    out[4 * h + 2] = t.z;
+                    out[4 * h + 3] = t.w;
+                } else {
+                    out[4 * h] += t.x;
+                    out[4 * h + 1] += t.y;
+                    out[4 * h + 2] += t.z;
+                    out[4 * h + 3] += t.w;
+                }
+            }
+        }
+#pragma unroll
+        for (int j = 0; j < 16; ++j) out[j] *= P.alpha;
+        finish_chunk<kN>(P, tm, tn, tm * kTile + rr, chunk, out, nullptr);
+    }
+    ptx::cluster_sync();  // peers may still read this CTA's partial
+}
+
 template <int kFmt, int kN = 128, bool kSplit = false>
 __global__ void __launch_bounds__(GemmTraits<kFmt, kN>::kThreads, GemmTraits<kFmt, kN>::kMinBlocks)
     umma_gemm_kernel(const __grid_constant__ GemmBatch batch) {
@@ -438,7 +507,10 @@ __global__ void __launch_bounds__(GemmTraits<kFmt, kN>::kThreads, GemmTraits<kFm
     uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(cbar + 1);
     float* col_scale = reinterpret_cast<float*>(tail + 256);  // kOZ8: 2^e_b per tile column
 
-    const int gt = blockIdx.x;
+    // kBF16 split-K: the CTAs of one cluster share a tile, CTA rank = k-slice
+    const int ks = kFmt == kBF16 && batch.k_split > 1 ? batch.k_split : 1;
+    const int gt = static_cast<int>(blockIdx.x) / ks;
+    const int kslice = static_cast<int>(blockIdx.x) % ks;
     int p = 0, lt;
     if (batch.interleave) {
         p = gt % batch.n_probs;
@@ -455,8 +527,13 @@ __global__ void __launch_bounds__(GemmTraits<kFmt, kN>::kThreads, GemmTraits<kFm
     if (P.k_mode == K_FROM_COL_TILE) k_begin = tn * kTile;
     if (P.k_mode == K_TO_ROW_TILE_END) k_end = min(P.k, (tm + 1) * kTile);
     if (P.k_mode == K_TO_COL_TILE_END) k_end = min(P.k, (tn + 1) * kTile);
-    const int kb0 = k_begin / T::kKBlock;
-    const int kb1 = max(kb0, (k_end + T::kKBlock - 1) / T::kKBlock);
+    int kb0 = k_begin / T::kKBlock;
+    int kb1 = max(kb0, (k_end + T::kKBlock - 1) / T::kKBlock);
+    if (ks > 1) {  // contiguous k-block slices, the last ones possibly shorter / empty
+        const int per = (kb1 - kb0 + ks - 1) / ks;
+        kb0 = min(kb1, kb0 + kslice * per);
+        kb1 = min(kb1, kb0 + per);
+    }
 
     const int warp = threadIdx.x >> 5;
     const uint32_t lane = threadIdx.x & 31;
@@ -600,7 +677,15 @@ __global__ void __launch_bounds__(GemmTraits<kFmt, kN>::kThreads, GemmTraits<kFm
     ptx::grid_dep_launch();  // main loop done: let the next launch start its prologue
     if (cpre) ptx::mbar_wait(cbar, 0);
     __syncwarp();
-    {
+    bool split_k = false;
+    if constexpr (kFmt == kBF16) {
+        static_assert(kTile * (kN + 4) * 4 <= kStages * T::kStageBytes, "split-K tile does not fit the stages");
+        if (ks > 1) {
+            split_k_epilogue<kN, T::kThreads>(P, tm, tn, smem, tmem, ks, kslice, have_acc);
+            split_k = true;
+        }
+    }
+    if (!split_k) {
         constexpr int kPairs = T::kThreads / 128;  // warps sharing a TMEM lane quarter
         const int ew = warp & 3, part = warp >> 2;
         constexpr int kChunks = kN / 16 / kPairs;

@@ -132,7 +132,9 @@ class CudaBackend:
         self.graph_fb = bool(graph_fb) and not self.recompute_on
         self.graphed: Dict[Tuple[int, int, bool], object] = {}
         self.inv_graphs: Dict[Tuple[int, ...], torch.cuda.CUDAGraph] = {}  # batched inversions (graph_fb)
-        self.cur_step = 0  # set by the executor before each op (trace metadata)
+        self.cur_step = 0  # set by the executor before each op (trace metadata):
+        self.cur_op = None  # program index of the op (first of a batched run)
+        self.cur_gate = None  # program index of the F/B op it is gated on
 
     # ------------------------------------------------------------ timing helpers
     def _begin(self, stream):
@@ -148,6 +150,8 @@ class CudaBackend:
         e1 = torch.cuda.Event(enable_timing=True)
         e1.record(stream)
         meta.setdefault("step", self.cur_step)
+        meta.setdefault("op", self.cur_op)
+        meta.setdefault("gate", self.cur_gate)
         self.timeline.append((kind, e0, e1, meta))
 
     def mark_compute(self):
@@ -749,6 +753,95 @@ def measured_trace(trainer: "PipeFisherTrainer") -> dict:
             "otherData": {"source": "measured: CUDA events around each op on its stream (batched items = one event)",
                           "cycle_ms": span, "refresh_steps": trainer.refresh,
                           "util_reference_definition": busy_sum / span if span > 0 else 0.0}}
+
+
+def _overlap(a, b, iv):
+    """Length of [a, b] covered by the sorted, disjoint intervals iv."""
+    return sum(max(0.0, min(b, e) - max(a, s)) for s, e in iv if e > a and s < b)
+
+
+def _union(iv):
+    out = []
+    for s, e in sorted(iv):
+        if out and s <= out[-1][1]:
+            out[-1][1] = max(out[-1][1], e)
+        else:
+            out.append([s, e])
+    return [(s, e) for s, e in out]
+
+
+def bubble_landing(program, trace, cycle_ms: float) -> dict:
+    """Where the K-FAC items of one recorded cycle actually ran against the
+    bubbles the assigner gave them (bubblefill.cpp:286-344 places each item in
+    a gap of its device's timeline; runtime._assign_gates turns that gap into
+    'after F/B op g, before the next F/B op').
+
+    program: the device program (runtime.Op list, schedule-time costs);
+    trace: [(kind, start_ms, end_ms, meta)] of run_cycle(record=True), meta
+    carrying the program index ('op') and gate ('gate') of each event.
+
+    Per bubble (the gate op): its planned length (schedule units), its
+    measured length (end of the gate F/B -> start of the next F/B on the
+    compute stream, or the cycle end), the K-FAC time that ran inside it and
+    the part that spilled past it (running beside the next F/B).  Totals: the
+    fraction of K-FAC time inside its own bubble, the fraction that overlapped
+    ANY F/B, and the count of items that started before their gate ended (a
+    dependency violation; must be 0)."""
+    fb = {}
+    for kind, a, b, m in trace:
+        if kind in COMPUTE_KINDS and m.get("op") is not None:
+            s, e = fb.get(m["op"], (a, b))
+            fb[m["op"]] = (min(s, a), max(e, b))
+    fb_iv = _union(fb.values())
+    compute_idx = [i for i, o in enumerate(program) if o.kind in COMPUTE_KINDS]
+    bubbles: Dict[object, dict] = {}
+    eps = 1e-3  # ms: event timestamp resolution
+    early = 0
+    for kind, a, b, m in trace:
+        if kind not in KFAC_KINDS:
+            continue
+        g = m.get("gate")
+        b0 = fb[g][1] if g is not None and g in fb else 0.0
+        nxt = next((i for i in compute_idx if g is None or i > g), None)
+        b1 = fb[nxt][0] if nxt is not None and nxt in fb else cycle_ms
+        if g is not None and nxt is not None:
+            go, no = program[g], program[nxt]
+            planned = no.start - (go.start + go.duration)
+        elif nxt is not None:
+            planned = program[nxt].start
+        else:
+            planned = None
+        if a < b0 - eps:
+            early += 1
+        bub = bubbles.setdefault(g, {"gate": g, "next": nxt, "planned": planned, "measured_ms": max(0.0, b1 - b0),
+                                     "begin": b0, "end": b1, "items": 0, "iv": [], "kinds": []})
+        bub["items"] += int(m.get("items", 1))
+        bub["iv"].append((a, b))
+        bub["kinds"].append(kind)
+    rows, k_total, k_inside, k_fb = [], 0.0, 0.0, 0.0
+    for g in sorted(bubbles, key=lambda x: -1 if x is None else x):
+        bub = bubbles[g]
+        iv = _union(bub.pop("iv"))
+        busy = sum(e - s for s, e in iv)
+        inside = sum(_overlap(bub["begin"], bub["end"], [(s, e)]) for s, e in iv)
+        with_fb = sum(_overlap(s, e, fb_iv) for s, e in iv)
+        k_total, k_inside, k_fb = k_total + busy, k_inside + inside, k_fb + with_fb
+        bub.update(kfac_ms=busy, inside_ms=inside, spill_ms=busy - inside, kinds=sorted(set(bub["kinds"])))
+        rows.append(bub)
+    return {"bubbles": rows, "kfac_ms": k_total,
+            "inside_fraction": k_inside / k_total if k_total > 0 else 1.0,
+            "fb_overlap_fraction": k_fb / k_total if k_total > 0 else 0.0,
+            "started_before_gate": early}
+
+
+def trainer_bubble_landing(trainer: "PipeFisherTrainer") -> dict:
+    """bubble_landing of this rank's last run_cycle(record=True)."""
+    return bubble_landing(trainer.program, getattr(trainer, "last_trace", []),
+                          getattr(trainer, "last_cycle_ms", 0.0))
+
+
+COMPUTE_KINDS = ("F", "RECOMP", "B")
+KFAC_KINDS = ("CURV", "SYNC_CURV", "INV")
 
 
 class _LocalComm:

@@ -360,7 +360,7 @@ class Executor:
         i = 0
         while i < len(prog):
             op = prog[i]
-            b.cur_step = op.step  # trace metadata
+            b.cur_step, b.cur_op, b.cur_gate = op.step, i, op.gate  # trace metadata
             # a run of consecutive Curvature / Inversion items behind the same
             # gate becomes ONE backend call (one grouped SYRK launch / one
             # batched inverse whose independent chains overlap)

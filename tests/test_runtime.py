@@ -283,3 +283,43 @@ def test_pipeline_projection_from_measured_costs():
     assert r["cost_table"]["t_f"] == 3.0 and r["cost_table"]["t_inv"] == 6.0
     assert r["pipefisher_step_ms"] >= r["plain_step_ms"] and r["refresh_period"] >= 1
     assert 0.0 < r["simulated_util"] <= 1.0
+
+
+@pytest.mark.parametrize("name,method,D,N,W,L", CASES)
+def test_bubble_landing_of_an_on_schedule_trace(name, method, D, N, W, L):
+    """engine.bubble_landing maps each recorded K-FAC event to the bubble its
+    gate names.  A trace that runs every op exactly at its schedule time (ms =
+    schedule units) lands all K-FAC time inside its bubbles with no F/B
+    overlap; stretching one item past the next F/B start shows up as spill."""
+    from paper_2211_14133_b200.engine import bubble_landing
+    _, filled, progs = build(method, D, N, W, L)
+    span = filled.schedule.makespan if hasattr(filled.schedule, "makespan") else \
+        max(o.start + o.duration for p in progs for o in p)
+    for p in progs:
+        trace = []
+        for i, o in enumerate(p):
+            if o.kind in (R.F_, R.B_, R.CURV, R.SYNC_CURV, R.INV):
+                trace.append((o.kind, o.start, o.start + o.duration, {"op": i, "gate": o.gate}))
+        rep = bubble_landing(p, trace, span)
+        n_kfac = sum(o.kind in R.KFAC_STREAM_OPS for o in p)
+        assert sum(b["items"] for b in rep["bubbles"]) == n_kfac
+        assert rep["started_before_gate"] == 0
+        if rep["kfac_ms"] > 0:
+            assert rep["inside_fraction"] == pytest.approx(1.0, abs=1e-9)
+            assert rep["fb_overlap_fraction"] == pytest.approx(0.0, abs=1e-9)
+        for b in rep["bubbles"]:
+            if b["planned"] is not None and b["next"] is not None:
+                assert b["measured_ms"] == pytest.approx(b["planned"], abs=1e-9)
+        # one curvature item overruns its bubble by 0.5 units
+        j = next((k for k, (kind, a, b, m) in enumerate(trace)
+                  if kind == R.CURV and m["gate"] is not None and
+                  any(q.kind in R.COMPUTE_OPS for q in p[m["gate"] + 1:])), None)
+        if j is None:
+            continue
+        kind, a, b, m = trace[j]
+        nxt = next(i for i in range(m["gate"] + 1, len(p)) if p[i].kind in R.COMPUTE_OPS)
+        trace[j] = (kind, a, p[nxt].start + 0.5, m)
+        rep = bubble_landing(p, trace, span)
+        spill = sum(bb["spill_ms"] for bb in rep["bubbles"])
+        assert spill == pytest.approx(0.5, abs=1e-9)
+        assert rep["fb_overlap_fraction"] > 0

@@ -141,3 +141,32 @@ def test_1f1b_d2_w2_data_parallel():
     # W = 2 data-parallel groups see DIFFERENT data, yet SyncCurvature and
     # SyncGrad make every stage's replicas identical after each cycle
     _replicas_identical(out, out[0][0].topo)
+
+
+def test_chimera_d4_kfac_landing_recorded():
+    """Where the K-FAC items land against their assigned bubbles (measured CUDA
+    events of a recorded cycle, engine.bubble_landing): every item accounted
+    for, none starts before the F/B op it is gated on.  The virtual devices
+    share one GPU's SMs, so the lengths are not a multi-GPU measurement; with
+    PF_LANDING_OUT set the per-rank reports are written there as JSON."""
+    import json
+    import os
+    from paper_2211_14133_b200 import runtime as R
+    from paper_2211_14133_b200.engine import trainer_bubble_landing
+    bert = tiny(8)
+    cfg = S.PipelineConfig(method=S.Method.Chimera, stages=4, micro_batches=4, micro_batch_size=4, seq_len=64,
+                           layers_per_stage=2, replicas=2)
+    out, _ = run(cfg, bert, cycles=2, record=True)
+    reports = []
+    for t, res in out:
+        rep = trainer_bubble_landing(t)
+        n_kfac = sum(o.kind in R.KFAC_STREAM_OPS for o in t.program)
+        assert sum(b["items"] for b in rep["bubbles"]) == n_kfac
+        assert rep["started_before_gate"] == 0
+        assert 0.0 <= rep["inside_fraction"] <= 1.0
+        reports.append({"rank": t.rank, "cycle_ms": t.last_cycle_ms, **rep})
+    path = os.environ.get("PF_LANDING_OUT")
+    if path:
+        with open(path, "w") as f:
+            json.dump({"config": "Chimera D=4 W=2 (virtual devices on one B200), tiny BERT", "ranks": reports},
+                      f, indent=1)

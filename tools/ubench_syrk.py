@@ -20,9 +20,13 @@ def timed(fn, iters=20):
     with torch.cuda.stream(s):
         fn()
     torch.cuda.current_stream().wait_stream(s)
+    # PF_UB_PER_GRAPH=n: n calls captured back to back in one graph (no
+    # per-graph launch gap between them); default 1 call per graph
+    per = int(os.environ.get("PF_UB_PER_GRAPH", "1"))
     g = torch.cuda.CUDAGraph()
     with torch.cuda.graph(g):
-        fn()
+        for _ in range(per):
+            fn()
     for _ in range(3):
         g.replay()
     torch.cuda.synchronize()
@@ -32,7 +36,7 @@ def timed(fn, iters=20):
         g.replay()
     e1.record()
     torch.cuda.synchronize()
-    return e0.elapsed_time(e1) / iters
+    return e0.elapsed_time(e1) / iters / per
 
 
 def main():
