@@ -338,14 +338,15 @@ int make_desc(const GemmSpec& s, GemmDesc& d, CUtensorMap* maps, int n_maps) {
     };
     std::memset(&d, 0, sizeof(d));
     d.a_map = put_maps(true);
-    d.b_map = shared_ab && kN == kTile ? d.a_map : put_maps(false);  // B box is kN rows
+    // (bf16 boxes are 128 rows for both operands; digit-plane B boxes are kN rows)
+    d.b_map = shared_ab && (kFmt == kBF16 || kN == kTile) ? d.a_map : put_maps(false);
     if (kFmt == kOZ8 && shared_ab) d.flags |= EPI_EXACT_DIAG;
     d.rows = s.rows;
     d.cols = s.cols;
     d.k = s.k;
     d.tiles_m = (s.rows + kTile - 1) / kTile;
     d.tiles_n = (s.cols + kN - 1) / kN;
-    d.lower = s.lower ? 1 : 0;
+    d.lower = s.lower ? (kN == 2 * kTile ? 2 : 1) : 0;  // 2: 128 x 256 lower tiles
     d.k_mode = s.k_mode;
     d.alpha = s.alpha;
     d.beta = s.beta;
@@ -365,7 +366,13 @@ int make_desc(const GemmSpec& s, GemmDesc& d, CUtensorMap* maps, int n_maps) {
     return m - n_maps;
 }
 
-inline int desc_tiles(const GemmDesc& d) { return d.lower ? d.tiles_m * (d.tiles_m + 1) / 2 : d.tiles_m * d.tiles_n; }
+inline int desc_tiles(const GemmDesc& d) {
+    if (d.lower == 2) {  // row tile tm holds tm / 2 + 1 tiles of 256 columns
+        const int a = d.tiles_m / 2;
+        return a * (a + 1) + (d.tiles_m % 2 ? a + 1 : 0);
+    }
+    return d.lower ? d.tiles_m * (d.tiles_m + 1) / 2 : d.tiles_m * d.tiles_n;
+}
 
 int sm_count();
 
@@ -500,7 +507,7 @@ void launch_gemms_n(const std::vector<GemmSpec>& specs_in, cudaStream_t stream) 
                 continue;
             }
         }
-        if constexpr (kFmt == kBF16) {
+        if constexpr (kFmt == kBF16 && kN == kTile) {
             batch.k_split = bf16_k_split(batch, tiles);
             if (batch.k_split > 1) {
                 launch_cluster(kernel, dim3(tiles * batch.k_split), dim3(T::kThreads), T::kSmemBytes, stream,
@@ -549,7 +556,25 @@ int pick_tile_n(const std::vector<GemmSpec>& specs) {
     return kTile;
 }
 
-void gemm_bf16(const std::vector<GemmSpec>& s, cudaStream_t st) { launch_gemms_n<kBF16, 128>(s, st); }
+// bf16 (SYRK) launches: 128 x 256 tiles when the launch has more 128-wide
+// tiles than SMs -- one CTA pulls operands from L2 at ~100-120 GB/s, and a
+// 256-wide tile does twice the MMAs of a 128-wide one for 1.5x the bytes --
+// otherwise 128-wide tiles, split over k (bf16_k_split) when they are few.
+// PF_SYRK_WIDE=0: always 128-wide; =2: always 256-wide (tests).
+void gemm_bf16(const std::vector<GemmSpec>& s, cudaStream_t st) {
+    static const int wide = [] { const char* e = std::getenv("PF_SYRK_WIDE"); return e ? std::atoi(e) : 1; }();
+    long tiles = 0;
+    bool all_lower = true;
+    for (const GemmSpec& g : s) {
+        const long tm = (g.rows + kTile - 1) / kTile;
+        tiles += g.lower ? tm * (tm + 1) / 2 : tm * ((g.cols + kTile - 1) / kTile);
+        all_lower = all_lower && g.lower && g.k_mode == K_FULL;
+    }
+    if (all_lower && (wide == 2 || (wide == 1 && tiles > sm_count())))
+        launch_gemms_n<kBF16, 2 * kTile>(s, st);
+    else
+        launch_gemms_n<kBF16, kTile>(s, st);
+}
 void gemm_oz8(const std::vector<GemmSpec>& s, cudaStream_t st) {
     if (!s.empty() && (s.front().flags & EPI_DIAG_SPLIT)) {  // the LAUUM (mirrored: 128-wide tiles)
         for (const GemmSpec& g : s)

@@ -119,6 +119,9 @@ struct GemmDesc {
                          // activations [tokens x features]); two 64-wide TMA boxes per tile
 };
 
+// MN-major bf16 operand tiles: 64-feature groups of 64 tokens x 128 B
+constexpr int kMnGroupBytes = 64 * 128;
+
 struct GemmBatch {
     CUtensorMap maps[kMaxMaps];
     GemmDesc probs[kMaxProbs];
@@ -139,7 +142,8 @@ struct GemmTraits {
     static constexpr int kPlaneBytes = kFmt == kOZ8 ? 128 * 64 : 128 * 128;  // A plane (128 rows)
     static constexpr int kPlaneBytesB = kFmt == kOZ8 ? kN * 64 : kN * 128;   // B plane (kN rows)
     static constexpr int kStageBytes = kPlanes * (kPlaneBytes + kPlaneBytesB);
-    static constexpr int kStages = 3;
+    // bf16 128x256 tiles (48 KB per stage) keep two CTAs per SM with 2 stages each
+    static constexpr int kStages = kFmt == kBF16 && kN == 256 ? 2 : 3;
     // C-tile prefetch buffer (beta != 0, <= kStages-1 k-blocks): the unused
     // last stage plus kCPad, rows padded to kCStride floats (bank rotation)
     static constexpr int kCStride = kN + 4;
@@ -148,7 +152,7 @@ struct GemmTraits {
     static constexpr int kSmemBytes = kStages * kStageBytes + kCPad + 1024 + 256 + 4 * kTile;
     static constexpr int kKBlock = 64;  // elements per k-block (both formats)
     static constexpr int kKSteps = kFmt == kOZ8 ? 2 : 4;  // 32-byte UMMA k-steps per block
-    static constexpr uint32_t kTmemCols = kFmt == kOZ8 ? 4 * kN : 128;
+    static constexpr uint32_t kTmemCols = kFmt == kOZ8 ? 4 * kN : kN;
     static constexpr int kMinBlocks = kFmt == kOZ8 ? 1 : 2;
     // kOZ8 (one CTA per SM: 512 TMEM columns) runs 8 warps so the 4-accumulator
     // epilogue is split over warp pairs sharing a TMEM lane quarter
@@ -161,10 +165,15 @@ struct GemmTraits {
 };
 
 __device__ __forceinline__ void decode_lower(int t, int& tm, int& tn);
+__device__ __forceinline__ void decode_lower_wide(int t, int& tm, int& tn);
 
 // Local tile index -> (tm, tn), longest k-range first (LPT): with triangular
 // k-ranges the last wave would otherwise wait on the longest tiles.
 __device__ __forceinline__ void map_tile(const GemmDesc& P, int lt, int& tm, int& tn) {
+    if (P.lower == 2) {  // 128 x 256 tiles (kBF16 kN = 256), K_FULL
+        decode_lower_wide(lt, tm, tn);
+        return;
+    }
     if (P.lower) {  // decode_lower walks tm ascending: K_FROM_ROW_TILE longest first
         decode_lower(lt, tm, tn);
         return;
@@ -185,6 +194,23 @@ __device__ __forceinline__ void map_tile(const GemmDesc& P, int lt, int& tm, int
         default:
             tm = lt / P.tiles_n;
             tn = lt % P.tiles_n;
+    }
+}
+
+// Lower tiles of 128 rows x 256 columns: row tile tm has tm / 2 + 1 of them
+// (the last one holds the 128 x 128 diagonal block, plus the block right of
+// it when tm is even -- never stored); rows 2a and 2a+1 start at a (a + 1).
+__device__ __forceinline__ void decode_lower_wide(int t, int& tm, int& tn) {
+    int a = static_cast<int>((sqrtf(4.0f * static_cast<float>(t) + 1.0f) - 1.0f) * 0.5f);
+    while ((a + 1) * (a + 2) <= t) ++a;
+    while (a * (a + 1) > t) --a;
+    const int r = t - a * (a + 1);
+    if (r <= a) {
+        tm = 2 * a;
+        tn = r;
+    } else {
+        tm = 2 * a + 1;
+        tn = r - a - 1;
     }
 }
 
@@ -230,9 +256,13 @@ __device__ __forceinline__ void finish_chunk(const GemmDesc& P, int tm, int tn, 
                                              const float* crow) {
     const uint32_t f = P.flags;
     const bool row_ok = r < P.rows;
-    const bool mirror = (f & EPI_MIRROR) && tm != tn;
     const int c0 = tn * kN + chunk * 16;
-    if (!row_ok || c0 >= P.cols) return;
+    // 128-wide column block of the chunk (== tn for 128-wide tiles): a lower
+    // launch never stores blocks right of the diagonal block, and mirrors the
+    // ones left of it
+    const int cb = c0 / kTile;
+    if (!row_ok || c0 >= P.cols || (P.lower && cb > tm)) return;
+    const bool mirror = (f & EPI_MIRROR) && cb != tm;
     const bool full_chunk = c0 + 16 <= P.cols;
     if (P.beta != 0.0f) {
         float cv[16];
@@ -508,7 +538,7 @@ __global__ void __launch_bounds__(GemmTraits<kFmt, kN>::kThreads, GemmTraits<kFm
     float* col_scale = reinterpret_cast<float*>(tail + 256);  // kOZ8: 2^e_b per tile column
 
     // kBF16 split-K: the CTAs of one cluster share a tile, CTA rank = k-slice
-    const int ks = kFmt == kBF16 && batch.k_split > 1 ? batch.k_split : 1;
+    const int ks = kFmt == kBF16 && kN == kTile && batch.k_split > 1 ? batch.k_split : 1;
     const int gt = static_cast<int>(blockIdx.x) / ks;
     const int kslice = static_cast<int>(blockIdx.x) % ks;
     int p = 0, lt;
@@ -597,14 +627,18 @@ __global__ void __launch_bounds__(GemmTraits<kFmt, kN>::kThreads, GemmTraits<kFm
                 ptx::tma_load_3d(a_plane(s, 0), &batch.maps[P.a_map], &full[s], kc, tm * kTile, 0);
                 ptx::tma_load_3d(b_plane(s, 0), &batch.maps[P.b_map], &full[s], kc, tn * kN, 0);
             } else if (P.mn_major) {
-                // box {64 features, 64 tokens} per half: [half][token][64 features]
+                // box {64 features, 64 tokens} per 64-feature group: [group][token][64 features]
                 ptx::tma_load_2d(a_plane(s, 0), &batch.maps[P.a_map], &full[s], tm * kTile, kc);
-                ptx::tma_load_2d(a_plane(s, 0) + T::kPlaneBytes / 2, &batch.maps[P.a_map], &full[s], tm * kTile + 64, kc);
-                ptx::tma_load_2d(b_plane(s, 0), &batch.maps[P.b_map], &full[s], tn * kN, kc);
-                ptx::tma_load_2d(b_plane(s, 0) + T::kPlaneBytesB / 2, &batch.maps[P.b_map], &full[s], tn * kN + 64, kc);
+                ptx::tma_load_2d(a_plane(s, 0) + kMnGroupBytes, &batch.maps[P.a_map], &full[s], tm * kTile + 64, kc);
+#pragma unroll
+                for (int h = 0; h < kN / 64; ++h)
+                    ptx::tma_load_2d(b_plane(s, 0) + h * kMnGroupBytes, &batch.maps[P.b_map], &full[s], tn * kN + 64 * h, kc);
             } else {
+                // box {64 elements, 128 rows}; a 256-row B tile is two boxes
                 ptx::tma_load_2d(a_plane(s, 0), &batch.maps[P.a_map], &full[s], kc, tm * kTile);
-                ptx::tma_load_2d(b_plane(s, 0), &batch.maps[P.b_map], &full[s], kc, tn * kN);
+#pragma unroll
+                for (int h = 0; h < (kN + kTile - 1) / kTile; ++h)
+                    ptx::tma_load_2d(b_plane(s, 0) + h * kTile * 128, &batch.maps[P.b_map], &full[s], kc, tn * kN + kTile * h);
             }
             if (++s == kStages) {
                 s = 0;
@@ -636,8 +670,8 @@ __global__ void __launch_bounds__(GemmTraits<kFmt, kN>::kThreads, GemmTraits<kFm
                     // 16 K rows per UMMA = two 8-row groups of 1024 B
                     const uint32_t moff = ks * 2048;
                     ptx::umma_f16(tmem,
-                                  ptx::sw128_mnmajor_desc(ptx::smem_u32(a_plane(s, 0)) + moff, T::kPlaneBytes / 2, 1024),
-                                  ptx::sw128_mnmajor_desc(ptx::smem_u32(b_plane(s, 0)) + moff, T::kPlaneBytesB / 2, 1024),
+                                  ptx::sw128_mnmajor_desc(ptx::smem_u32(a_plane(s, 0)) + moff, kMnGroupBytes, 1024),
+                                  ptx::sw128_mnmajor_desc(ptx::smem_u32(b_plane(s, 0)) + moff, kMnGroupBytes, 1024),
                                   T::kIdesc | ptx::kIdescAMnMajor | ptx::kIdescBMnMajor, started);
                     started = 1;
                 } else {
@@ -678,7 +712,7 @@ __global__ void __launch_bounds__(GemmTraits<kFmt, kN>::kThreads, GemmTraits<kFm
     if (cpre) ptx::mbar_wait(cbar, 0);
     __syncwarp();
     bool split_k = false;
-    if constexpr (kFmt == kBF16) {
+    if constexpr (kFmt == kBF16 && kN == kTile) {
         static_assert(kTile * (kN + 4) * 4 <= kStages * T::kStageBytes, "split-K tile does not fit the stages");
         if (ks > 1) {
             split_k_epilogue<kN, T::kThreads>(P, tm, tn, smem, tmem, ks, kslice, have_acc);

@@ -117,3 +117,48 @@ def test_forced_split_factors(ks):
             assert v, k
         else:
             assert v <= 1e-5, (k, v)
+
+
+WIDE_SNIPPET = r"""
+import json, sys, torch
+sys.path.insert(0, %r)
+from paper_2211_14133_b200 import kfac as K
+out = {}
+cases = ((384, 512, False, True), (200, 136, False, True), (640, 1024, True, True), (1024, 4096, True, False),
+         (4096, 512, False, True))
+for d, n, tm, fill in cases:
+    g = torch.Generator(device="cuda").manual_seed(d + n)
+    x = torch.randn((n, d) if tm else (d, n), generator=g, device="cuda").to(torch.bfloat16)
+    f = torch.full((d, d), 0.5, device="cuda")
+    K.syrk([(x, f, 1.0 / n, True, tm)], fill_upper=fill)
+    torch.cuda.synchronize()
+    xd = x.double()
+    w = 0.5 + ((xd.t() @ xd) if tm else (xd @ xd.t())) / n
+    key = "%%d_%%d_%%d_%%d" %% (d, n, tm, fill)
+    blk = torch.arange(d, device="cuda") // 128
+    low = blk[None, :] <= blk[:, None]  # 128-blocks on or left of the diagonal block
+    out[key] = float((f.double() - w)[low].norm() / w[low].norm())
+    if fill:
+        out["sym_" + key] = bool(torch.equal(f, f.t())) and float((f.double() - w).norm() / w.norm()) <= 1e-5
+    else:
+        out["sym_" + key] = bool(torch.equal(f[~low], torch.full_like(f[~low], 0.5)))  # never written
+print(json.dumps(out))
+""" % ROOT
+
+
+@pytest.mark.parametrize("wide", ["0", "2"])
+def test_wide_tiles_forced(wide):
+    """PF_SYRK_WIDE=2 runs every SYRK on 128 x 256 tiles (default: launches of
+    more 128-wide tiles than SMs): ragged d with a 256-wide tile whose second
+    128-row B box lies wholly past d (d = 384), partial tiles (d = 200),
+    token-major operands, accumulate, lower-only (blocks right of the diagonal
+    block never written) and the mirrored upper triangle."""
+    env = dict(os.environ, PF_SYRK_WIDE=wide)
+    out = subprocess.run([sys.executable, "-c", WIDE_SNIPPET], env=env, capture_output=True, text=True, timeout=600)
+    assert out.returncode == 0, out.stderr[-2000:]
+    res = json.loads(out.stdout.strip().splitlines()[-1])
+    for k, v in res.items():
+        if k.startswith("sym_"):
+            assert v, k
+        else:
+            assert v <= 1e-5, (k, v)
