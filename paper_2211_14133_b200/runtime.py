@@ -262,9 +262,12 @@ def _assign_gates(p: List[Op]):
 def inline_program(cfg: S.PipelineConfig, refresh: int) -> List[Op]:
     """D = 1, W = 1: no bubbles.  Step k of an R-step cycle: 1F1B order F/B
     (with cfg.recompute, a Recompute of the micro-batch glued in front of its
-    Backward, reference schedule.cpp:188-189, :215-223), then (k == 0)
-    Curvature for every (layer, set, micro) and Inversion for every
-    (layer, set), then Precondition."""
+    Backward, reference schedule.cpp:188-189, :215-223); in step 0 the
+    Curvature items of micro-batch m (every layer and set) right after m's
+    Backward -- its A and B tapes are complete there, so they run on the
+    K-FAC stream beside the remaining F/B instead of after the step (same
+    items, same micro-batch order per factor: the same bits); then
+    Inversion for every (layer, set), then Precondition."""
     if cfg.stages != 1:
         raise ValueError("inline_program is the single-stage (D = 1) case")
     n, L = cfg.micro_batches, cfg.layers_per_stage
@@ -277,11 +280,11 @@ def inline_program(cfg: S.PipelineConfig, refresh: int) -> List[Op]:
         for kind, m in fb:
             prog.append(Op(kind, 0, k, t, 1.0, m))
             t += 1.0
-        if k == 0:
-            for m in range(n):
+            if k == 0 and kind == B_:
                 for l in range(L):
                     for f in (0, 1):
                         prog.append(Op(CURV, 0, k, t, 0.0, m, l, f))
+        if k == 0:
             for l in range(L):
                 for f in (0, 1):
                     prog.append(Op(INV, 0, k, t, 0.0, None, l, f))

@@ -124,6 +124,14 @@ def test_inline_program_single_device():
     # 1F1B on one device: F0 B0 F1 B1 ...
     fb = [(o.kind, o.micro) for o in prog if o.kind in (R.F_, R.B_) and o.step == 0]
     assert fb == [(R.F_, 0), (R.B_, 0), (R.F_, 1), (R.B_, 1), (R.F_, 2), (R.B_, 2), (R.F_, 3), (R.B_, 3)]
+    # step 0: micro-batch m's curvature items right after its backward (gated on it)
+    for i, o in enumerate(prog):
+        if o.kind == R.CURV:
+            g = prog[o.gate]
+            assert (g.kind, g.micro, g.step) == (R.B_, o.micro, 0)
+    inv = [i for i, o in enumerate(prog) if o.kind == R.INV]
+    last_b0 = max(i for i, o in enumerate(prog) if o.kind == R.B_ and o.step == 0)
+    assert min(inv) > last_b0 and all(prog[i].gate == last_b0 for i in inv)
     with pytest.raises(ValueError):
         R.inline_program(S.PipelineConfig(stages=2, micro_batches=2), 1)
     rc = R.inline_program(S.PipelineConfig(stages=1, micro_batches=3, layers_per_stage=2, recompute=True), 1)

@@ -44,6 +44,9 @@ def main():
                                             "op_ms_per_cycle": {k: {"ops": v[0], "ms": round(v[1], 3)} for k, v in kinds.items()},
                                             "cycle_ms": r.step_ms * t.refresh,
                                             "cupti": kernel_activity(t)}
+        if os.environ.get("PF_D1_TRACE") == "1":  # the recorded cycle's op intervals (ms from cycle start)
+            out["kfac" if kfac else "plain"]["trace"] = [(k, round(a, 2), round(b, 2), m.get("step"))
+                                                         for k, a, b, m in getattr(t, "last_trace", [])]
         del t
         torch.cuda.empty_cache()
     print(json.dumps(out, indent=1))
