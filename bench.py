@@ -218,9 +218,8 @@ class LayerStep:
         self.grads = [torch.randn((do, di), generator=g, device="cuda") for _, di, do in LINEARS]
         self.weights = [0.02 * torch.randn((do, di), generator=g, device="cuda") for _, di, do in LINEARS]
 
-    def curvature(self, which=None):
-        idx = range(len(self.factors)) if which is None else which
-        self.K.syrk([(self.tapes[i], self.factors[i], 1.0 / TOKENS, False, True) for i in idx],
+    def curvature(self):
+        self.K.syrk([(x, f, 1.0 / TOKENS, False, True) for x, f in zip(self.tapes, self.factors)],
                     fill_upper=False)
 
     def invert(self, which=None):
@@ -231,10 +230,10 @@ class LayerStep:
                                           [self.inv[i] for i in idx],
                                           [self.digits[i] for i in idx], check=False)
 
-    def precondition(self, which=None):
+    def precondition(self):
         K = self.K
         items = []
-        for l in (range(len(LINEARS)) if which is None else which):
+        for l in range(len(LINEARS)):
             ai = K.SlicedMatrix(self.inv[2 * l], self.digits[2 * l])
             bi = K.SlicedMatrix(self.inv[2 * l + 1], self.digits[2 * l + 1])
             items.append((self.weights[l], self.grads[l], ai, bi, ETA))
@@ -321,50 +320,11 @@ def run_gpu_arm(args, rank, world, local_rank):
     def exchange():
         sync_factors(torch, dist, st.factors, tril)
 
-    # Single GPU: the layer's work as a two-stream DAG.  The critical path is
-    # the 4096-wide factors' chain (SYRK -> inverse -> the ffn1 / ffn2
-    # preconditions that read them); the 1024-wide factors' SYRK + inverse and
-    # the q / k / v / o preconditions (1024-wide inverses only) run beside it
-    # on a second stream in background mode (least launch priority, no
-    # persistent CTAs), so they fill the SMs the chain leaves idle instead of
-    # sitting before / after it.  --no-dag: one stream, phase after phase.
-    dag = world == 1 and not args.no_dag
-    big = [i for i, f in enumerate(st.factors) if f.shape[0] > D_MODEL]
-    small = [i for i in range(len(st.factors)) if i not in big]
-    lin_small = [l for l in range(len(LINEARS)) if 2 * l in small and 2 * l + 1 in small]
-    lin_big = [l for l in range(len(LINEARS)) if l not in lin_small]
-    side = torch.cuda.Stream()
-    small_inv_done = torch.cuda.Event()
-
     def step(ev=None):
-        if dag and ev is None:
-            dag_a()
-            dag_b()
-            stream.wait_stream(side)
-            return
         step_a(ev)
         step_b(ev)
 
-    def dag_a():
-        side.wait_stream(stream)
-        with torch.cuda.stream(side), K.background():
-            st.curvature(small)
-            st.invert(small)
-        small_inv_done.record(side)
-        st.curvature(big)
-        st.invert(big)
-
-    def dag_b():
-        with torch.cuda.stream(side), K.background():
-            st.precondition(lin_small)
-        stream.wait_event(small_inv_done)
-        st.precondition(lin_big)
-
     def step_a(ev=None):  # needs the tapes
-        if dag and ev is None:  # (the e2e graphs: the small inversions joined before the gradients' part)
-            dag_a()
-            stream.wait_stream(side)
-            return
         if ev: ev[0].record(stream)
         st.curvature()
         if ev: ev[1].record(stream)
@@ -381,11 +341,6 @@ def run_gpu_arm(args, rank, world, local_rank):
         if ev: ev[2].record(stream)
 
     def step_b(ev=None):  # needs the gradients
-        if dag and ev is None:
-            side.wait_stream(stream)
-            dag_b()
-            stream.wait_stream(side)
-            return
         st.precondition()
         if ev: ev[3].record(stream)
 
@@ -436,7 +391,6 @@ def run_gpu_arm(args, rank, world, local_rank):
     # are host-bound when issued eagerly).  Otherwise an eager pass with events
     # between the phases.
     phases = {"curvature": 0.0, "inversion": 0.0, "precondition": 0.0}
-    one_stream_ms = None
     if graphed:
         def prefix_graph(fn):
             g = torch.cuda.CUDAGraph()
@@ -458,13 +412,8 @@ def run_gpu_arm(args, rank, world, local_rank):
             torch.cuda.synchronize()
             return e0.elapsed_time(e1) / args.steps
 
-        # (with the DAG schedule the phases overlap: each is measured as a
-        # one-stream prefix, the whole one-stream step included)
-        g_all = prefix_graph(lambda: (st.curvature(), st.invert(), st.precondition())) if dag else graph
-        t_c, t_ci, t_all = replay_ms(g_c), replay_ms(g_ci), replay_ms(g_all)
+        t_c, t_ci, t_all = replay_ms(g_c), replay_ms(g_ci), replay_ms(graph)
         phases = {"curvature": t_c, "inversion": t_ci - t_c, "precondition": t_all - t_ci}
-        if dag:
-            one_stream_ms = t_all
     else:
         evs = [[torch.cuda.Event(enable_timing=True) for _ in range(4)] for _ in range(args.steps)]
         for i in range(args.steps):
@@ -685,11 +634,6 @@ def run_gpu_arm(args, rank, world, local_rank):
                    "l2": "inputs larger than L2 (tapes 144 MB + factors 168 MB per step)"},
         "phases": phase_rates,
         "cuda_graph": graphed,
-        "schedule": ("two-stream DAG: 4096-wide factors' SYRK -> inverse -> ffn1/ffn2 precondition on the "
-                     "main stream, the 1024-wide factors' SYRK + inverse + q/k/v/o precondition beside it "
-                     "(background mode); phases below are each timed alone on one stream") if dag else
-                    "one stream, phase after phase",
-        "one_stream_ms_per_step": one_stream_ms,
         "roofline": roof,
         "roofline_syrk": roof_syrk,
         "roofline_precondition": roof_prec,
@@ -810,8 +754,6 @@ def main():
     p.add_argument("--impl", default="ours", choices=["ours", "reference"])
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--no-graph", action="store_true", help="eager launches instead of a CUDA graph")
-    p.add_argument("--no-dag", action="store_true",
-                   help="single GPU: run the layer step on one stream, phase after phase")
     p.add_argument("--no-pipeline", action="store_true", help="skip the BERT-Large pipeline step section")
     args = p.parse_args()
     rank = int(os.environ.get("RANK", "0"))
