@@ -556,21 +556,27 @@ int pick_tile_n(const std::vector<GemmSpec>& specs) {
     return kTile;
 }
 
-// bf16 (SYRK) launches: 128 x 256 tiles when the launch has more 128-wide
-// tiles than SMs -- one CTA pulls operands from L2 at ~100-120 GB/s, and a
-// 256-wide tile does twice the MMAs of a 128-wide one for 1.5x the bytes --
-// otherwise 128-wide tiles, split over k (bf16_k_split) when they are few.
-// PF_SYRK_WIDE=0: always 128-wide; =2: always 256-wide (tests).
+// bf16 (SYRK) launches: 128 x 256 or 128 x 128 tiles, whichever needs fewer
+// wave-times.  Both keep two CTAs per SM; all tiles of a SYRK launch have the
+// same K, so a launch takes ceil(tiles / (2 SMs)) waves, and a 256-wide wave
+// takes ~1.75x a 128-wide one (measured: d = 4096 alone, 1 wide wave 60 us
+// against 2 narrow waves 69 us; the grouped 12-factor layer launch, 3 wide
+// waves against 5 narrow, is ~2 % faster narrow).  Few 128-wide tiles: split
+// over k instead (bf16_k_split).  PF_SYRK_WIDE=0: never 256-wide; =2: always.
 void gemm_bf16(const std::vector<GemmSpec>& s, cudaStream_t st) {
     static const int wide = [] { const char* e = std::getenv("PF_SYRK_WIDE"); return e ? std::atoi(e) : 1; }();
-    long tiles = 0;
+    long narrow_tiles = 0, wide_tiles = 0;
     bool all_lower = true;
     for (const GemmSpec& g : s) {
-        const long tm = (g.rows + kTile - 1) / kTile;
-        tiles += g.lower ? tm * (tm + 1) / 2 : tm * ((g.cols + kTile - 1) / kTile);
+        const long tm = (g.rows + kTile - 1) / kTile, a = tm / 2;
+        narrow_tiles += g.lower ? tm * (tm + 1) / 2 : tm * ((g.cols + kTile - 1) / kTile);
+        wide_tiles += a * (a + 1) + (tm % 2 ? a + 1 : 0);
         all_lower = all_lower && g.lower && g.k_mode == K_FULL;
     }
-    if (all_lower && (wide == 2 || (wide == 1 && tiles > sm_count())))
+    const long slots = 2L * sm_count();
+    const long nn = (narrow_tiles + slots - 1) / slots, nw = (wide_tiles + slots - 1) / slots;
+    const bool use_wide = all_lower && (wide == 2 || (wide == 1 && narrow_tiles > sm_count() && 7 * nw < 4 * nn));
+    if (use_wide)
         launch_gemms_n<kBF16, 2 * kTile>(s, st);
     else
         launch_gemms_n<kBF16, kTile>(s, st);

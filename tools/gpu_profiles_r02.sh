@@ -15,14 +15,17 @@ run timeout 900 python bench.py --steps 20 --warmup 5
 grep '^{' $OUT/log.txt | tail -1 > $OUT/bench.json
 run timeout 300 ncu --profile-from-start off --metrics gpu__time_duration.sum --clock-control none --csv \
     --log-file $OUT/launches.csv python tools/prof_phase.py step 2
-cap() {  # name phase kernel-regex skip
+cap() {  # name phase kernel-regex skip   (CAPS="name ..." limits the captures: gpurun copies back <= 64 MiB)
+  if [ -n "${CAPS:-}" ] && ! echo " $CAPS " | grep -q " $1 "; then return; fi
   run timeout 600 ncu --profile-from-start off --set full --clock-control none --import-source on --kernel-name-base mangled \
       -k "regex:$3" -s ${4:-0} -c 1 -o $OUT/$1 python tools/prof_phase.py $2 1
 }
 cap syrk curvature 'umma_gemm_kernelILi1ELi256'
 # split-K SYRK (single d = 1024 factor: 2-CTA clusters), from the SYRK probe
+if [ -z "${CAPS:-}" ] || echo " $CAPS " | grep -q " syrk_splitk "; then
 run timeout 600 ncu --set full --clock-control none --import-source on --kernel-name-base mangled \
     -k "regex:umma_gemm_kernelILi1ELi128" -s 6 -c 1 -o $OUT/syrk_splitk python tools/probe/syrk_small.py
+fi
 cap prec precondition 'umma_gemm_persist_kernelILb0'
 cap gemm32 inversion 'umma_gemm_kernelILi3ELi32E' 20
 cap gemm64 inversion 'umma_gemm_kernelILi3ELi64E' 10
