@@ -237,7 +237,18 @@ struct SliceReq {
     int ld;
     int mode;
     Sliced dst;
+    const int* ready = nullptr;  // SliceJob::ready (slice_short only; the others wait for the launch)
 };
+
+// PF_READY_FLAGS=0: the chain's X_kk slice waits for the leaf launch to
+// complete instead of for its published X (A/B switch)
+bool ready_flags_enabled() {
+    static const bool on = [] {
+        const char* e = std::getenv("PF_READY_FLAGS");
+        return !(e && e[0] == '0');
+    }();
+    return on;
+}
 
 bool warp_slice_2k() {  // PF_WARP_SLICE_2K=0: rows of 1025..2048 by the block-per-row kernel (A/B)
     static const bool on = [] {
@@ -263,7 +274,7 @@ void launch_slices(const std::vector<SliceReq>& reqs, cudaStream_t st) {
         for (int j = 0; j < cnt; ++j) {
             const SliceReq& r = reqs[i + j];
             b.j[j] = SliceJob{r.src, r.dst.rows, r.dst.k, r.ld, r.mode, r.dst.planes,
-                              r.dst.plane_stride, r.dst.kpad, r.dst.exps, r.dst.sqnorm};
+                              r.dst.plane_stride, r.dst.kpad, r.dst.exps, r.dst.sqnorm, r.ready};
             rows = std::max(rows, r.dst.rows);
             kmax = std::max(kmax, r.dst.k);
         }
@@ -698,6 +709,7 @@ struct InvWs {
     void* px[3] = {};
     void* pl[3] = {};
     int* info = nullptr;
+    int* ready = nullptr;   // one flag per 128-column panel (LeafArgs::ready)
     float* lout = nullptr;  // pf_cholesky_factor: leaves also write their block of L here
     int ldl = 0;
 };
@@ -724,7 +736,8 @@ size_t inverse_ws_bytes(int d) {
     size_t side = 0;
     for (int n1 : node_n1_bounds(d)) side += 2 * align256(sliced_bytes(n1, n1));
     const size_t panel = 2 * align256(sliced_bytes(d, kLeaf)) + align256(sliced_bytes(kLeaf, kLeaf));
-    return 4 * plane + tplane + 2 * align256(sliced_bytes(d, d)) + side + 3 * panel;
+    const size_t flags = align256(static_cast<size_t>((d + kLeaf - 1) / kLeaf) * sizeof(int));
+    return 4 * plane + tplane + 2 * align256(sliced_bytes(d, d)) + side + 3 * panel + flags;
 }
 
 InvWs carve(void* base, int d) {
@@ -759,6 +772,7 @@ InvWs carve(void* base, int d) {
         w.px[i] = q;
         q += align256(sliced_bytes(kLeaf, kLeaf));
     }
+    w.ready = reinterpret_cast<int*>(q);  // reset by each leaf before use: no initialisation needed
     return w;
 }
 
@@ -774,7 +788,9 @@ struct Emitter {
     virtual void damp(const std::vector<Damp2D>& jobs) = 0;
     virtual void slices(const std::vector<SliceReq>& reqs) = 0;
     virtual void gemms(const std::vector<GemmSpec>& specs) = 0;
-    virtual void leaves(const std::vector<InvWs>& ws, int o, int n) = 0;
+    // publish: each leaf releases its panel's `ready` flag once X is stored
+    // (the right-looking chain's slice of X_kk starts on it)
+    virtual void leaves(const std::vector<InvWs>& ws, int o, int n, bool publish = false) = 0;
     // work emitted between side_begin(k) and side_end(k) may run concurrently
     // with what follows on the main chain until side_join(k)
     virtual void side_begin(int) {}
@@ -914,7 +930,7 @@ struct StreamEmitter final : Emitter {
         ScopedPrio sp(prio);
         gemm_oz8(specs, st);
     }
-    void leaves(const std::vector<InvWs>& ws, int o, int n) override {
+    void leaves(const std::vector<InvWs>& ws, int o, int n, bool publish = false) override {
         ScopedPrio sp(prio);
         static std::once_flag once;
         std::call_once(once, [] {
@@ -931,6 +947,7 @@ struct StreamEmitter final : Emitter {
             bool with_l = false;
             for (int j = 0; j < cnt; ++j) {
                 b.e[j] = leaf_args(ws[i + j], o, n);
+                if (publish && ready_flags_enabled()) b.e[j].ready = ws[i + j].ready + o / kLeaf;
                 with_l = with_l || b.e[j].l;
             }
             if (with_l) {
@@ -1148,14 +1165,17 @@ void cholesky_blocked(const std::vector<InvWs>& ws, Emitter& em,
     for (int k = 0; k < nb; ++k) {
         const int o = k * kLeaf;
         em.mark_lead(k, nb);
-        em.leaves(ws, o, std::min(kLeaf, d - o));
+        em.leaves(ws, o, std::min(kLeaf, d - o), true);
         if (after_leaf) after_leaf(k);
         if (k == nb - 1) break;
         const int r0 = o + kLeaf, m = d - r0, slot = k % 3;
         const int nc = std::min(kLeaf, m);  // width of block column k+1
         sl.clear();
         g.clear();
-        for (const InvWs& w : ws) sl.push_back(slice_of(w.x, w.ld, o, o, kLeaf, kLeaf, w.px[slot], SLICE_FULL));
+        for (const InvWs& w : ws) {
+            sl.push_back(slice_of(w.x, w.ld, o, o, kLeaf, kLeaf, w.px[slot], SLICE_FULL));
+            if (ready_flags_enabled()) sl.back().ready = w.ready + k;  // starts on the leaf's X, not its end
+        }
         em.slices(sl);
         if (k >= 1) em.wait(evA(k));  // A panel of k (col of k-1)
         // ---- TRSM: L[r0:, k] = A[r0:, k] X_kk^T

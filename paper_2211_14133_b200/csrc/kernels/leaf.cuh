@@ -100,6 +100,10 @@ struct LeafArgs {
     int col0;  // global column of the block (for info)
     float* l = nullptr;  // optional: the block's Cholesky factor L_kk (lower part only; pf_cholesky_factor)
     int ldl = 0;
+    // optional: published (set to 1, release) once X is in global memory, before
+    // X^T is stored; reset at the start.  The slice of X_kk on the right-looking
+    // chain waits on it instead of on this launch's completion.
+    int* ready = nullptr;
 };
 
 struct LeafBatch {
@@ -457,8 +461,17 @@ __device__ __forceinline__ void zero_upper_blocks(float* Xs) {
 // x = X (lower, zeros above) and xt = X^T for the n x n block
 // `tbuf` (pitch kLeafPitch, 128 rows) is scratch: the active-matrix buffer,
 // free once the factorisation is done.  Every thread must call this.
-__device__ __forceinline__ void store_x(const float* Xs, float* tbuf, float* x, float* xt, int ld, int n) {
+__device__ __forceinline__ void store_x(const float* Xs, float* tbuf, float* x, float* xt, int ld, int n,
+                                        int* ready = nullptr) {
     const int tid = threadIdx.x;
+    auto publish = [&] {  // every thread's X stores, then one release of the flag
+        if (!ready) return;
+        __syncthreads();
+        if (tid == 0) {
+            __threadfence();
+            atomicExch(ready, 1);
+        }
+    };
     const bool vec = n == kLeaf && (ld % 4 == 0) && ((reinterpret_cast<uintptr_t>(x) & 15) == 0) &&
                      ((reinterpret_cast<uintptr_t>(xt) & 15) == 0);
     if (vec) {
@@ -479,6 +492,7 @@ __device__ __forceinline__ void store_x(const float* Xs, float* tbuf, float* x, 
                 *reinterpret_cast<float4*>(x + (size_t)r * ld + c) = v[q];
             }
         }
+        publish();
         // X^T: transpose into the (now free) pitch-129 buffer, then store its rows
         for (int idx = tid; idx < kLeaf * kLeaf; idx += kLeafThreads) {
             const int r = idx / kLeaf, c = idx % kLeaf;  // lanes: consecutive c
@@ -496,6 +510,7 @@ __device__ __forceinline__ void store_x(const float* Xs, float* tbuf, float* x, 
             x[(size_t)r * ld + c] = Xs[r * kXPitch + c];
             xt[(size_t)r * ld + c] = Xs[c * kXPitch + r];
         }
+        publish();
     }
 }
 
@@ -568,7 +583,10 @@ __device__ __forceinline__ void leaf_body(const LeafArgs& A, float* leaf_smem, b
 #ifdef PF_LEAF_RING
     long long r_t0 = leaf_gtimer(), r_c0 = clock64(), r_t1 = 0, r_t2 = 0;
 #endif
-    if (tid == 0) *bad = INT_MAX;
+    if (tid == 0) {
+        *bad = INT_MAX;
+        if (A.ready) atomicExch(A.ready, 0);  // performed at L2 before any reader can start (below)
+    }
     if (pdl) ptx::grid_dep_wait();  // PDL: A is produced by the previous launch
 #ifdef PF_LEAF_RING
     r_t1 = leaf_gtimer();
@@ -668,7 +686,7 @@ __device__ __forceinline__ void leaf_body(const LeafArgs& A, float* leaf_smem, b
     const long long r_t3 = leaf_gtimer();
 #endif
     if (pdl) ptx::grid_dep_launch();
-    store_x(Xs, Ls, A.x, A.xt, A.ld, A.n);
+    store_x(Xs, Ls, A.x, A.xt, A.ld, A.n, A.ready);
     PF_STAMP(19);
 #ifdef PF_LEAF_RING
     __syncthreads();

@@ -40,6 +40,11 @@ struct SliceJob {
     int kpad;
     int* exps;
     double* sqnorm;
+    // optional: the rows are published by their producer with this flag (set
+    // to 1) before the producer's launch completes (the leaf's X, ahead of its
+    // X^T store); slice_short waits on it instead of on the launch and joins
+    // the launch at its end, so its own completion still implies the producer's
+    const int* ready = nullptr;
 };
 
 constexpr int kMaxSliceJobs = 32;
@@ -372,7 +377,13 @@ __global__ void __launch_bounds__(256) slice_short_kernel(const __grid_constant_
     const SliceJob& J = b.j[blockIdx.y];
     const int g = threadIdx.x & (kLanes - 1);                              // lane within the row group
     const int r = blockIdx.x * (256 / kLanes) + threadIdx.x / kLanes;  // row
-    ptx::grid_dep_wait();
+    if (J.ready) {
+        if (threadIdx.x == 0)
+            while (ptx::ld_acquire_gpu(J.ready) == 0) __nanosleep(64);
+        __syncthreads();
+    } else {
+        ptx::grid_dep_wait();
+    }
     ptx::grid_dep_launch();
     const bool live = r < J.rows;
     int lo = 0, hi = 0;
@@ -417,6 +428,7 @@ __global__ void __launch_bounds__(256) slice_short_kernel(const __grid_constant_
         J.exps[r] = e;
         J.sqnorm[r] = sq.value();
     }
+    if (J.ready) ptx::grid_dep_wait();  // complete only after the producer's launch
 }
 
 // one warp per row; grid (ceil(rows / 8), jobs)
