@@ -31,7 +31,11 @@ def _worker(rank, world, port, q):
         bench.sync_factors(torch, dist, factors, tril)
         digits = [torch.full((5 + i,), float(10 * rank + i)).to(torch.uint8) for i in range(len(dims))]
         bench.share_inverses(dist, digits, world)
-        q.put((rank, [f.clone() for f in factors], upper_before, [d.clone() for d in digits]))
+        # numpy copies travel by value: tensors would go through shared-memory
+        # fds that vanish if this process exits before the parent unpickles
+        # them (an intermittent ConnectionResetError)
+        q.put((rank, [f.numpy().copy() for f in factors], [u.numpy().copy() for u in upper_before],
+               [d.numpy().copy() for d in digits]))
     finally:
         dist.destroy_process_group()
 
@@ -47,7 +51,7 @@ def test_packed_factor_allreduce_and_digit_broadcast():
     res = {}
     for _ in range(world):
         r, f, up, dg = q.get(timeout=120)
-        res[r] = (f, up, dg)
+        res[r] = tuple([torch.from_numpy(a) for a in lst] for lst in (f, up, dg))
     for p in procs:
         p.join(timeout=60)
         assert p.exitcode == 0
