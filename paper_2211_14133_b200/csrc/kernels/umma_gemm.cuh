@@ -934,6 +934,18 @@ __global__ void __launch_bounds__(kPersistThreads, 1)
                 col_scale[et] = c < P.cols ? ptx::pow2f(__ldcg(P.b_exp + c)) : 0.0f;
             }
             const int r = tm * kTile + ew * 32 + static_cast<int>(lane);
+            if (P.beta != 0.0f && r < P.rows && !(P.flags & EPI_TRANSPOSE)) {
+                // C (e.g. the weights of W -= eta P) is read only after this
+                // tile's MMAs: pull this thread's row segment into L2 now
+                const int c0 = tn * kTile + part * (kTile / 2);
+                if (c0 < P.cols) {
+                    const float* row = P.c + static_cast<size_t>(r) * P.ldc + c0;
+                    const int n = min(kTile / 2, P.cols - c0);
+#pragma unroll
+                    for (int j = 0; j < kTile / 2; j += 32)
+                        if (j < n) ptx::prefetch_l2(row + j);
+                }
+            }
             const EpiRow er = epi_row<kOZ8, kTile, kSplit>(P, tm, tn, r);
             asm volatile("bar.sync 1, 256;" ::: "memory");
             ptx::mbar_wait(done, it & 1);
