@@ -564,9 +564,10 @@ def run_gpu_arm(args, rank, world, local_rank):
 
     check = self_check(torch, st, step_a, step_b,
                        owned=None if world == 1 else {i for i in range(len(st.factors)) if i % world == rank})
-    pipeline = None if args.no_pipeline else pipeline_section(args, rank, world, local_rank, dist)
-
     if rank != 0:
+        if not args.no_pipeline:
+            with _Watchdog(world, None):
+                pipeline_section(args, rank, world, local_rank, dist)
         if dist: dist.destroy_process_group()
         return
 
@@ -644,10 +645,44 @@ def run_gpu_arm(args, rank, world, local_rank):
         "gpu_launches": launches,
         "clocks": clocks.summary(),
         "cpu_baseline": cpu,
-        "pipeline": pipeline,
+        "pipeline": None,
     }
+    if not args.no_pipeline:
+        with _Watchdog(world, line):
+            line["pipeline"] = pipeline_section(args, rank, world, local_rank, dist)
     print(json.dumps(line), flush=True)
     if dist: dist.destroy_process_group()
+
+
+class _Watchdog:
+    """N > 1: the pipeline section runs real NCCL point-to-point programs
+    across ranks; if one rank fails inside them the others block in a
+    collective for good.  After PF_BENCH_PIPE_TIMEOUT seconds (default 600)
+    every rank exits, rank 0 first printing the bench line with the pipeline
+    section marked as timed out -- a hang there never swallows the layer-step
+    measurement.  N = 1 runs unguarded."""
+
+    def __init__(self, world, line):
+        self.world, self.line, self.timer = world, line, None
+
+    def _fire(self):
+        if self.line is not None:
+            self.line["pipeline"] = {"error": "timed out (a rank failed or hung inside the pipeline programs)"}
+            print(json.dumps(self.line), flush=True)
+        os._exit(0)
+
+    def __enter__(self):
+        if self.world > 1:
+            import threading
+            self.timer = threading.Timer(float(os.environ.get("PF_BENCH_PIPE_TIMEOUT", "600")), self._fire)
+            self.timer.daemon = True
+            self.timer.start()
+        return self
+
+    def __exit__(self, *exc):
+        if self.timer is not None:
+            self.timer.cancel()
+        return False
 
 
 # ====================================================================== pipeline step
