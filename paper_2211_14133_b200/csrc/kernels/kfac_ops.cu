@@ -250,6 +250,20 @@ bool ready_flags_enabled() {
     return on;
 }
 
+// PF_DIAG_FP32=0: the right-looking chain's diagonal update of block k+1 as
+// slice(L) + a one-tile digit GEMM on the chain (round-2 schedule) instead
+// of one fp32 SIMT launch (diag_update_kernel) reading the TRSM's fp32
+// output, the slice of L moved to the side branch.  Changes results by
+// rounding (fp32 FMA sums instead of exact digit products; inverse residual
+// 2.02e-6 vs 2.04e-6 at d = 4096).
+bool diag_fp32_enabled() {
+    static const bool on = [] {
+        const char* e = std::getenv("PF_DIAG_FP32");
+        return !(e && e[0] == '0');
+    }();
+    return on;
+}
+
 bool warp_slice_2k() {  // PF_WARP_SLICE_2K=0: rows of 1025..2048 by the block-per-row kernel (A/B)
     static const bool on = [] {
         const char* e = std::getenv("PF_WARP_SLICE_2K");
@@ -620,6 +634,62 @@ struct DampBatch {
     Damp2D e[kMaxDamp];
 };
 
+constexpr int kDiagTiles = 36;
+struct DiagUpd {
+    const float* l;
+    float* a;
+    int ld;
+    int n;
+};
+struct DiagBatch {
+    DiagUpd e[kMaxLeafBatch];
+};
+__global__ void __launch_bounds__(256) diag_update_kernel(const __grid_constant__ DiagBatch b) {
+    __shared__ float sa[kLeaf][33], sb[kLeaf][33];
+    const DiagUpd& P = b.e[blockIdx.y];
+    int ti = 0, tj = blockIdx.x;
+    while (tj > ti) tj -= ++ti;
+    const int tid = threadIdx.x;
+    ptx::grid_dep_wait();
+    ptx::grid_dep_launch();
+    if (32 * tj >= P.n) return;
+    float va[16], vb[16];
+#pragma unroll
+    for (int q = 0; q < 16; ++q) {
+        const int r = (tid >> 5) + 8 * (q & 3), k = (tid & 31) + 32 * (q >> 2);
+        const int ra = 32 * ti + r, rb = 32 * tj + r;
+        va[q] = ra < P.n ? __ldcg(P.l + (size_t)ra * P.ld + k) : 0.0f;
+        vb[q] = rb < P.n ? __ldcg(P.l + (size_t)rb * P.ld + k) : 0.0f;
+    }
+#pragma unroll
+    for (int q = 0; q < 16; ++q) {
+        const int r = (tid >> 5) + 8 * (q & 3), k = (tid & 31) + 32 * (q >> 2);
+        sa[k][r] = va[q];
+        sb[k][r] = vb[q];
+    }
+    __syncthreads();
+    const int ri = 2 * (tid >> 4), cj = 2 * (tid & 15);
+    float acc[2][2] = {{0.f, 0.f}, {0.f, 0.f}};
+#pragma unroll 16
+    for (int k = 0; k < kLeaf; ++k) {
+        const float a0 = sa[k][ri], a1 = sa[k][ri + 1], b0 = sb[k][cj], b1 = sb[k][cj + 1];
+        acc[0][0] = fmaf(a0, b0, acc[0][0]);
+        acc[0][1] = fmaf(a0, b1, acc[0][1]);
+        acc[1][0] = fmaf(a1, b0, acc[1][0]);
+        acc[1][1] = fmaf(a1, b1, acc[1][1]);
+    }
+#pragma unroll
+    for (int u = 0; u < 2; ++u)
+#pragma unroll
+        for (int v = 0; v < 2; ++v) {
+            const int r = 32 * ti + ri + u, c = 32 * tj + cj + v;
+            if (r < P.n && c <= r) {
+                float* d = P.a + (size_t)r * P.ld + c;
+                *d = fmaf(-1.0f, acc[u][v], *d);
+            }
+        }
+}
+
 // dst = M + damping * I, lower triangle incl. diagonal (the rest is never
 // read; whole float4 groups are copied).  One warp per row, 8 rows per CTA.
 __global__ void __launch_bounds__(256) damp_kernel(const __grid_constant__ DampBatch b) {
@@ -791,6 +861,7 @@ struct Emitter {
     // publish: each leaf releases its panel's `ready` flag once X is stored
     // (the right-looking chain's slice of X_kk starts on it)
     virtual void leaves(const std::vector<InvWs>& ws, int o, int n, bool publish = false) = 0;
+    virtual void diag_updates(const std::vector<InvWs>& ws, int r0, int n, int c) = 0;
     // work emitted between side_begin(k) and side_end(k) may run concurrently
     // with what follows on the main chain until side_join(k)
     virtual void side_begin(int) {}
@@ -929,6 +1000,18 @@ struct StreamEmitter final : Emitter {
     void gemms(const std::vector<GemmSpec>& specs) override {
         ScopedPrio sp(prio);
         gemm_oz8(specs, st);
+    }
+    void diag_updates(const std::vector<InvWs>& ws, int r0, int n, int c) override {
+        ScopedPrio sp(prio);
+        for (std::size_t i = 0; i < ws.size(); i += kMaxLeafBatch) {
+            DiagBatch b{};
+            const int cnt = static_cast<int>(std::min<std::size_t>(kMaxLeafBatch, ws.size() - i));
+            for (int j = 0; j < cnt; ++j)
+                b.e[j] = DiagUpd{at(ws[i + j].l, ws[i + j].ld, r0, c), at(ws[i + j].a, ws[i + j].ld, r0, r0),
+                                 ws[i + j].ld, n};
+            launch(diag_update_kernel, dim3(kDiagTiles, cnt), dim3(256), 0, st, b);
+            after_launch("diag_update_kernel");
+        }
     }
     void leaves(const std::vector<InvWs>& ws, int o, int n, bool publish = false) override {
         ScopedPrio sp(prio);
@@ -1194,8 +1277,16 @@ void cholesky_blocked(const std::vector<InvWs>& ws, Emitter& em,
         em.gemms(g);
         sl.clear();
         g.clear();
+        // by d, so a factor's bits never depend on what else is in the call:
+        // below 2048 the digit path stays (8x1024 alone: 528 vs 540 us; the
+        // layer step is the same either way)
+        static const int dfp_min_d = [] {
+            const char* e = std::getenv("PF_DIAG_FP32_MIN_D");
+            return e ? std::atoi(e) : 2048;
+        }();
+        const bool dfp = diag_fp32_enabled() && d >= dfp_min_d;
         for (const InvWs& w : ws) sl.push_back(slice_of(w.l, w.ld, r0, o, m, kLeaf, w.pl[slot], SLICE_FULL));
-        em.slices(sl);
+        if (!dfp) em.slices(sl);
         if (k >= 1 && m > 0) em.wait(evU(k - 1));  // BU(k-1) wrote block column k+1
         const bool rest = m > kLeaf;
         const int side = 1 + (k & 1);
@@ -1204,6 +1295,7 @@ void cholesky_blocked(const std::vector<InvWs>& ws, Emitter& em,
             em.on(side);
             em.wait(evF);
             side_used[side - 1] = true;
+            if (dfp) em.slices(sl);
             const int m2 = m - kLeaf;  // rows below block k+1
             // col: A[r0+128:, k+1] -= L[r0+128:, k] L[k+1, k]^T, then the A panel of k+1
             for (const InvWs& w : ws) {
@@ -1241,6 +1333,10 @@ void cholesky_blocked(const std::vector<InvWs>& ws, Emitter& em,
             em.on(0);
         }
         // ---- diagonal block of k+1 (critical)
+        if (dfp) {
+            em.diag_updates(ws, r0, nc, o);
+            continue;
+        }
         for (const InvWs& w : ws) {
             const Sliced lp = sliced_view(w.pl[slot], m, kLeaf);
             g.push_back(update(w, rows_of(lp, 0, nc), rows_of(lp, 0, nc), nc, nc, r0, r0, false));
@@ -1874,7 +1970,17 @@ int pf_damped_inverse_batched(const pf_inverse_problem* problems, int count, voi
                 const char* e = std::getenv("PF_INV_GROUP");
                 return e ? std::max(1, std::atoi(e)) : 0;
             }();
-            const std::size_t per = forced ? static_cast<std::size_t>(forced) : recursive ? 4 : 8;
+            // lead-size problems of a right-looking call in groups of
+            // PF_INV_GROUP_LEAD (default 1 with the fp32 diagonal update:
+            // separate chains on forked streams, 2x4096 + 10x1024 2.394 ->
+            // 2.357 ms; with the digit diagonal update shared launches were
+            // faster); 0 = groups of <= 8 like the others
+            static const int lead_per = [] {
+                const char* e = std::getenv("PF_INV_GROUP_LEAD");
+                return e ? std::max(0, std::atoi(e)) : diag_fp32_enabled() ? 1 : 0;
+            }();
+            std::size_t per = forced ? static_cast<std::size_t>(forced) : recursive ? 4 : 8;
+            if (lead_per && !recursive && order[i]->d == order.front()->d) per = static_cast<std::size_t>(lead_per);
             const std::size_t m = j - i, parts = (m + per - 1) / per;
             for (std::size_t q = 0; q < parts; ++q)
                 groups.emplace_back(order.begin() + i + m * q / parts, order.begin() + i + m * (q + 1) / parts);

@@ -42,7 +42,8 @@ print(json.dumps({"sha": h.hexdigest()}))
 """ % ROOT
 
 SWITCHES = ["PF_NO_NSPLIT=1", "PF_NO_PRIO=1", "PF_GEMM_PERSIST=0", "PF_EARLY_TRTRI=0", "PF_EARLY_ROOT=0", "PF_INV_DELAY=0",
-            "PF_SLICE_SHORT=0", "PF_WARP_SLICE_2K=0", "PF_NO_PDL=1", "PF_TRTRI_SPINE=0", "PF_READY_FLAGS=0"]
+            "PF_SLICE_SHORT=0", "PF_WARP_SLICE_2K=0", "PF_NO_PDL=1", "PF_TRTRI_SPINE=0", "PF_READY_FLAGS=0",
+            "PF_INV_GROUP_LEAD=0"]
 
 
 def run(env_kv=None):
