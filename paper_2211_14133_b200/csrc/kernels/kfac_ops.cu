@@ -264,6 +264,14 @@ bool diag_fp32_enabled() {
     return on;
 }
 
+int diag_fp32_min_d() {
+    static const int v = [] {
+        const char* e = std::getenv("PF_DIAG_FP32_MIN_D");
+        return e ? std::atoi(e) : 2048;
+    }();
+    return v;
+}
+
 bool warp_slice_2k() {  // PF_WARP_SLICE_2K=0: rows of 1025..2048 by the block-per-row kernel (A/B)
     static const bool on = [] {
         const char* e = std::getenv("PF_WARP_SLICE_2K");
@@ -573,9 +581,12 @@ int pick_tile_n(const std::vector<GemmSpec>& specs) {
     const int sms = sm_count();
     // a launch of at most sms / f32 (sms / f64) 128-wide tiles splits them 4 (2)
     // ways; re-tuned in round 2 with the faster leaf (layer inversion 2.49 ->
-    // 2.44 ms against f32 = 4, f64 = 2); PF_NSPLIT32 / PF_NSPLIT64 override
-    static const int f32 = [] { const char* e = std::getenv("PF_NSPLIT32"); return e ? std::atoi(e) : 8; }();
-    static const int f64 = [] { const char* e = std::getenv("PF_NSPLIT64"); return e ? std::atoi(e) : 4; }();
+    // 2.44 ms against f32 = 4, f64 = 2) and again for the separate lead
+    // chains of the fp32 diagonal update (f32 = f64 = 16 against 8 / 4:
+    // layer 2.365 -> 2.331 ms, 4x4096 3.53 -> 3.36 ms); PF_NSPLIT32 /
+    // PF_NSPLIT64 override
+    static const int f32 = [] { const char* e = std::getenv("PF_NSPLIT32"); return e ? std::atoi(e) : 16; }();
+    static const int f64 = [] { const char* e = std::getenv("PF_NSPLIT64"); return e ? std::atoi(e) : 16; }();
     if (tiles * f32 <= sms) return 32;
     if (tiles * f64 <= sms) return 64;
     return kTile;
@@ -1280,11 +1291,7 @@ void cholesky_blocked(const std::vector<InvWs>& ws, Emitter& em,
         // by d, so a factor's bits never depend on what else is in the call:
         // below 2048 the digit path stays (8x1024 alone: 528 vs 540 us; the
         // layer step is the same either way)
-        static const int dfp_min_d = [] {
-            const char* e = std::getenv("PF_DIAG_FP32_MIN_D");
-            return e ? std::atoi(e) : 2048;
-        }();
-        const bool dfp = diag_fp32_enabled() && d >= dfp_min_d;
+        const bool dfp = diag_fp32_enabled() && d >= diag_fp32_min_d();
         for (const InvWs& w : ws) sl.push_back(slice_of(w.l, w.ld, r0, o, m, kLeaf, w.pl[slot], SLICE_FULL));
         if (!dfp) em.slices(sl);
         if (k >= 1 && m > 0) em.wait(evU(k - 1));  // BU(k-1) wrote block column k+1
@@ -1980,7 +1987,8 @@ int pf_damped_inverse_batched(const pf_inverse_problem* problems, int count, voi
                 return e ? std::max(0, std::atoi(e)) : diag_fp32_enabled() ? 1 : 0;
             }();
             std::size_t per = forced ? static_cast<std::size_t>(forced) : recursive ? 4 : 8;
-            if (lead_per && !recursive && order[i]->d == order.front()->d) per = static_cast<std::size_t>(lead_per);
+            if (lead_per && !recursive && order[i]->d == order.front()->d && order[i]->d >= diag_fp32_min_d())
+                per = static_cast<std::size_t>(lead_per);
             const std::size_t m = j - i, parts = (m + per - 1) / per;
             for (std::size_t q = 0; q < parts; ++q)
                 groups.emplace_back(order.begin() + i + m * q / parts, order.begin() + i + m * (q + 1) / parts);
